@@ -1,0 +1,877 @@
+// mknn_api.cu -- the engine handle and the C-ABI (include/mknn_b200.h).
+//
+// Orchestrates one tick of Engine.process_tick (engine.py:601-696) on the
+// device: rebuild decision (quadindex.py:231-246) -> build_index ->
+// index_objects -> index_queries -> search (first iteration + direction
+// loop) -> emission.  The only host synchronisations per tick are the issuer
+// range read (to size the radix sort) and the final metrics read.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mknn_b200.h"
+#include "mknn_internal.h"
+
+using namespace mknn;
+
+namespace {
+
+template <typename T>
+int grow(T*& p, int64_t& cap_elems, int64_t want) {
+  if (want <= cap_elems && p) return 0;
+  int64_t nc = std::max<int64_t>(want, std::max<int64_t>(cap_elems * 3 / 2, 1024));
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap_elems = 0;
+  MKNN_CUDA_OK(cudaMalloc(&p, sizeof(T) * (size_t)nc));
+  cap_elems = nc;
+  return 0;
+}
+
+struct Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= cap && p) return 0;
+    size_t nc = std::max(bytes, cap * 3 / 2);
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    MKNN_CUDA_OK(cudaMalloc(&p, nc));
+    cap = nc;
+    return 0;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+constexpr long long HASH_EMPTY = (long long)0x8000000000000000ULL;
+
+__device__ __forceinline__ uint64_t hash64(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ULL;
+  x ^= x >> 33;
+  return x;
+}
+
+__global__ void k_fill_i64(long long* p, int64_t n, long long v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+__global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+// id -> slot map (open addressing, linear probing).  A new id claims the
+// next snapshot slot; concurrent inserts of one id wait for the winner.
+__device__ int32_t hash_find_or_insert(long long* keys, int32_t* vals, uint64_t mask, long long id,
+                                       int32_t* n_snap, bool insert_new, int32_t fixed_slot) {
+  uint64_t h = hash64((uint64_t)id) & mask;
+  for (;;) {
+    long long cur = keys[h];
+    if (cur == id) {
+      int32_t v;
+      while ((v = ((volatile int32_t*)vals)[h]) < 0) {
+      }
+      return v;
+    }
+    if (cur == HASH_EMPTY) {
+      const long long prev = (long long)atomicCAS((unsigned long long*)&keys[h],
+                                                  (unsigned long long)HASH_EMPTY,
+                                                  (unsigned long long)id);
+      if (prev == HASH_EMPTY) {
+        const int32_t slot = insert_new ? (fixed_slot >= 0 ? fixed_slot : atomicAdd(n_snap, 1)) : -1;
+        __threadfence();
+        atomicExch(&vals[h], slot);
+        return slot;
+      }
+      if (prev == id) continue;  // lost the race to the same id: wait above
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+__global__ void k_hash_load(const long long* __restrict__ ids, int64_t n, long long* keys,
+                            int32_t* vals, uint64_t mask, int32_t* winner) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    // duplicate ids inside a snapshot: the first slot keeps the mapping
+    hash_find_or_insert(keys, vals, mask, ids[i], nullptr, true, (int32_t)i);
+  }
+}
+
+// last update per id wins (datasets.py:130-131): winner[slot] = max index
+__global__ void k_update_claim(const long long* __restrict__ ids, int64_t nu, long long* keys,
+                               int32_t* vals, uint64_t mask, int32_t* n_snap, int32_t* winner,
+                               int32_t* slot_of) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nu;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = hash_find_or_insert(keys, vals, mask, ids[i], n_snap, true, -1);
+    slot_of[i] = s;
+    atomicMax(&winner[s], (int32_t)i);
+  }
+}
+
+__global__ void k_update_apply(const long long* __restrict__ ids, const double* __restrict__ x,
+                               const double* __restrict__ y, int64_t nu,
+                               const int32_t* __restrict__ slot_of, int32_t* winner,
+                               long long* sids, double* sx, double* sy) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nu;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = slot_of[i];
+    if (winner[s] == (int32_t)i) {
+      sids[s] = ids[i];
+      sx[s] = x[i];
+      sy[s] = y[i];
+    }
+  }
+}
+
+__global__ void k_update_reset(int64_t nu, const int32_t* __restrict__ slot_of, int32_t* winner) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nu;
+       i += (int64_t)gridDim.x * blockDim.x)
+    winner[slot_of[i]] = -1;
+}
+
+inline unsigned gs_blocks(int64_t n) {
+  return (unsigned)std::min<int64_t>(std::max<int64_t>((n + 255) / 256, 1), 148 * 16);
+}
+
+int64_t us_between(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) return 0;
+  return (int64_t)llround(ms * 1000.0);
+}
+
+}  // namespace
+
+struct mknn_engine {
+  mknn_config cfg{};
+  Region r{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  std::string err;
+
+  DevIndex ix;
+  bool have_index = false;
+  int32_t h_l_deep = 0;
+  int64_t h_n_leaves = 0, h_overfull = 0, h_n_build = 0;
+  DevStore st;
+  DevQueries dq;
+
+  // staging for host-input ticks
+  long long* in_ids = nullptr; double *in_x = nullptr, *in_y = nullptr; int64_t cap_in = 0;
+  long long* in_qi = nullptr; double *in_qx = nullptr, *in_qy = nullptr; int64_t cap_qin = 0;
+  // padded result rows + CSR + per-query stats
+  int32_t* out_len = nullptr; int64_t cap_len = 0;
+  long long* out_nids = nullptr; double* out_dist = nullptr; int64_t cap_rows = 0;
+  long long* c_nids = nullptr; double* c_dist = nullptr; int64_t cap_c = 0;
+  int64_t* offsets = nullptr; int64_t cap_off = 0;
+  long long* out_qids = nullptr; int64_t cap_oq = 0;
+  QueryStats* stats = nullptr; int64_t cap_stats = 0;
+  unsigned long long* counters = nullptr;  // [0] evals [1] prunes [2] viol [3] clamped
+  uint32_t* hist = nullptr;                // 2 x hist_cap
+  int hist_cap = 0;
+  Buf scratch;
+
+  // persistent snapshot (delta path)
+  long long* snap_ids = nullptr; double *snap_x = nullptr, *snap_y = nullptr; int64_t cap_snap = 0;
+  int64_t n_snap = 0;
+  long long* hkeys = nullptr; int32_t* hvals = nullptr; int64_t hcap = 0;
+  int32_t* winner = nullptr; int64_t cap_winner = 0;
+  int32_t* slot_of = nullptr; int64_t cap_slot_of = 0;
+  int32_t* d_nsnap = nullptr;
+  long long* up_ids = nullptr; double *up_x = nullptr, *up_y = nullptr; int64_t cap_up = 0;
+
+  std::vector<int64_t> history;
+  int64_t tick = 0;
+  std::vector<int64_t> active[2];
+  cudaEvent_t ev[8] = {};
+
+  int set_err(int code) { return code; }
+  int invalid(const std::string& m) { return fail_msg(E_INVALID, m); }
+};
+
+namespace {
+
+int bind(mknn_engine* h) {
+  MKNN_CUDA_OK(cudaSetDevice(h->device));
+  return 0;
+}
+
+// quadindex.py:231-246 should_rebuild
+bool should_rebuild(const std::vector<int64_t>& c, int window, double factor) {
+  if ((int64_t)c.size() < window + 1) return false;
+  const int64_t last = c.back();
+  double sum = 0.0;
+  for (size_t i = c.size() - 1 - window; i < c.size() - 1; i++) sum += (double)c[i];
+  return (double)last > factor * (sum / window);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- core tick
+namespace {
+
+struct DevOut {
+  long long* qids;    // [nq] or nullptr
+  int32_t* len;       // [nq]
+  int64_t* offsets;   // [nq + 1]
+  long long* nids;    // CSR
+  double* dist;       // CSR
+};
+
+int alloc_store(mknn_engine* h, int64_t n) {
+  const int64_t ncap = int64_t(1) << (2 * h->cfg.l_max);
+  if (!h->st.cell_count) {
+    MKNN_CUDA_OK(cudaMalloc(&h->st.cell_count, sizeof(int32_t) * (ncap + 2)));
+    MKNN_CUDA_OK(cudaMalloc(&h->st.cell_start, sizeof(int32_t) * (ncap + 2)));
+    MKNN_CUDA_OK(cudaMalloc(&h->st.cell_fill, sizeof(int32_t) * (ncap + 2)));
+    MKNN_CUDA_OK(cudaMalloc(&h->dq.qcount, sizeof(int32_t) * (ncap + 2)));
+    MKNN_CUDA_OK(cudaMalloc(&h->dq.qstart, sizeof(int32_t) * (ncap + 2)));
+    MKNN_CUDA_OK(cudaMalloc(&h->dq.qfill, sizeof(int32_t) * (ncap + 2)));
+    MKNN_CUDA_OK(cudaMalloc(&h->dq.minmax, sizeof(int64_t) * 2));
+    MKNN_CUDA_OK(cudaMalloc(&h->counters, sizeof(unsigned long long) * 8));
+    h->hist_cap = (int)(ncap + 2);
+    MKNN_CUDA_OK(cudaMalloc(&h->hist, sizeof(uint32_t) * 2 * h->hist_cap));
+  }
+  if (n > h->st.cap) {
+    int64_t nc = std::max<int64_t>(n, h->st.cap * 3 / 2);
+    cudaFree(h->st.xy);
+    cudaFree(h->st.ids);
+    cudaFree(h->st.leaf);
+    h->st.xy = nullptr;
+    h->st.ids = nullptr;
+    h->st.leaf = nullptr;
+    h->st.cap = 0;
+    MKNN_CUDA_OK(cudaMalloc(&h->st.xy, sizeof(double2) * nc));
+    MKNN_CUDA_OK(cudaMalloc(&h->st.ids, sizeof(long long) * nc));
+    MKNN_CUDA_OK(cudaMalloc(&h->st.leaf, sizeof(uint32_t) * nc));
+    h->st.cap = nc;
+  }
+  return 0;
+}
+
+int alloc_queries(mknn_engine* h, int64_t nq) {
+  if (nq <= h->dq.cap) return 0;
+  const int64_t nc = std::max<int64_t>(nq, h->dq.cap * 3 / 2);
+  cudaFree(h->dq.leaf);
+  cudaFree(h->dq.order);
+  cudaFree(h->dq.row);
+  cudaFree(h->dq.keys);
+  cudaFree(h->dq.keys_alt);
+  cudaFree(h->dq.vals);
+  cudaFree(h->dq.vals_alt);
+  h->dq.cap = 0;
+  MKNN_CUDA_OK(cudaMalloc(&h->dq.leaf, sizeof(uint32_t) * nc));
+  MKNN_CUDA_OK(cudaMalloc(&h->dq.order, sizeof(uint32_t) * nc));
+  MKNN_CUDA_OK(cudaMalloc(&h->dq.row, sizeof(uint32_t) * nc));
+  MKNN_CUDA_OK(cudaMalloc(&h->dq.keys, sizeof(uint64_t) * nc));
+  MKNN_CUDA_OK(cudaMalloc(&h->dq.keys_alt, sizeof(uint64_t) * nc));
+  MKNN_CUDA_OK(cudaMalloc(&h->dq.vals, sizeof(uint32_t) * nc));
+  MKNN_CUDA_OK(cudaMalloc(&h->dq.vals_alt, sizeof(uint32_t) * nc));
+  h->dq.cap = nc;
+  return 0;
+}
+
+int refresh_index_info(mknn_engine* h) {
+  int32_t sc[8];
+  MKNN_CUDA_OK(cudaMemcpyAsync(sc, h->ix.scalars, sizeof(sc), cudaMemcpyDeviceToHost, h->stream));
+  MKNN_CUDA_OK(cudaStreamSynchronize(h->stream));
+  h->h_l_deep = sc[0];
+  h->h_n_leaves = sc[1];
+  h->h_overfull = sc[2];
+  h->h_n_build = sc[3];
+  return 0;
+}
+
+// Engine.process_tick over device-resident inputs; results into `o`.
+int core_tick(mknn_engine* h, int64_t n, const long long* ids, const double* x, const double* y,
+              int64_t nq, const long long* qi, const double* qx, const double* qy, const DevOut& o,
+              mknn_metrics* met, std::chrono::steady_clock::time_point t_start) {
+  const int k = h->cfg.k;
+  cudaStream_t s = h->stream;
+  int rc;
+  if ((rc = alloc_store(h, std::max<int64_t>(n, 1)))) return h->set_err(rc);
+  if ((rc = alloc_queries(h, std::max<int64_t>(nq, 1)))) return h->set_err(rc);
+  if ((rc = grow(h->stats, h->cap_stats, std::max<int64_t>(nq, 1)))) return h->set_err(rc);
+  const int64_t rows = std::max<int64_t>(nq * (int64_t)k, 1);
+  if (rows > h->cap_rows) {
+    int64_t c = h->cap_rows;
+    if ((rc = grow(h->out_nids, c, rows))) return h->set_err(rc);
+    c = h->cap_rows;
+    if ((rc = grow(h->out_dist, c, rows))) return h->set_err(rc);
+    h->cap_rows = c;
+  }
+  const int64_t ncap = int64_t(1) << (2 * h->cfg.l_max);
+  size_t sb = std::max({scan_scratch_bytes(ncap + 2), scan_scratch_bytes(std::max<int64_t>(nq, 1) + 1),
+                        radix_scratch_bytes(std::max<int64_t>(nq, 1))});
+  if ((rc = h->scratch.ensure(sb + 1024))) return h->set_err(rc);
+
+  mknn_metrics m{};
+  m.tick = h->tick;
+  m.n_objects = n;
+  m.n_queries = nq;
+
+  MKNN_CUDA_OK(cudaEventRecord(h->ev[0], s));
+  const bool rebuild =
+      !h->have_index || should_rebuild(h->history, h->cfg.rebuild_window, h->cfg.rebuild_factor);
+  if (rebuild) {
+    if ((rc = index_build(h->ix, h->r, x, y, n, h->scratch.p, s))) return h->set_err(rc);
+    h->have_index = true;
+    m.rebuild_flag = 1;
+  }
+  MKNN_CUDA_OK(cudaEventRecord(h->ev[1], s));
+  MKNN_CUDA_OK(cudaMemsetAsync(h->counters, 0, sizeof(unsigned long long) * 8, s));
+  if ((rc = store_index_objects(h->st, h->ix, h->r, ids, x, y, n, h->counters + 3, h->scratch.p, s)))
+    return h->set_err(rc);
+  MKNN_CUDA_OK(cudaEventRecord(h->ev[2], s));
+  if ((rc = queries_index(h->dq, h->ix, h->r, qi, qx, qy, nq, o.qids, h->scratch.p, s)))
+    return h->set_err(rc);
+  MKNN_CUDA_OK(cudaEventRecord(h->ev[3], s));
+
+  SearchArgs a{};
+  a.r = h->r;
+  a.k = k;
+  a.l_deep_host = -1;
+  a.scalars = h->ix.scalars;
+  a.z_map = h->ix.z_map;
+  a.leaf_key = h->ix.leaf_key;
+  a.leaf_span = h->ix.leaf_span;
+  a.cell_start = h->st.cell_start;
+  a.xy = h->st.xy;
+  a.ids = h->st.ids;
+  a.q_order = h->dq.order;
+  a.q_leaf = h->dq.leaf;
+  a.q_row = h->dq.row;
+  a.qi = qi;
+  a.qx = qx;
+  a.qy = qy;
+  a.nq = nq;
+  a.out_len = o.len;
+  a.out_nids = h->out_nids;
+  a.out_dist = h->out_dist;
+  a.stats = h->stats;
+  a.audit = h->cfg.audit_pruning;
+  if ((rc = search_launch(a, s))) return h->set_err(rc);
+  MKNN_CUDA_OK(cudaEventRecord(h->ev[4], s));
+  MKNN_CUDA_OK(cudaMemsetAsync(h->hist, 0, sizeof(uint32_t) * 2 * h->hist_cap, s));
+  if ((rc = stats_reduce(h->stats, nq, h->counters, h->hist, h->hist + h->hist_cap, h->hist_cap, s)))
+    return h->set_err(rc);
+  if ((rc = rows_compact(o.len, h->out_nids, h->out_dist, nq, k, o.offsets, o.nids, o.dist,
+                         h->scratch.p, s)))
+    return h->set_err(rc);
+  MKNN_CUDA_OK(cudaEventRecord(h->ev[5], s));
+
+  unsigned long long cnt[8];
+  MKNN_CUDA_OK(cudaMemcpyAsync(cnt, h->counters, sizeof(cnt), cudaMemcpyDeviceToHost, s));
+  int64_t total = 0;
+  MKNN_CUDA_OK(cudaMemcpyAsync(&total, o.offsets + nq, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  MKNN_CUDA_OK(cudaStreamSynchronize(s));
+  if (rebuild) {
+    if ((rc = refresh_index_info(h))) return h->set_err(rc);
+  }
+
+  // engine.py:661-663 active lists from navigate-call histograms
+  for (int d = 0; d < 2; d++) {
+    h->active[d].clear();
+    if (nq == 0) continue;
+    // fetch the histogram prefix that can be non-zero
+    std::vector<uint32_t> hh;
+    int64_t lim = std::min<int64_t>(h->hist_cap, 4096);
+    for (;;) {
+      hh.resize(lim);
+      MKNN_CUDA_OK(cudaMemcpy(hh.data(), h->hist + (int64_t)d * h->hist_cap, sizeof(uint32_t) * lim,
+                              cudaMemcpyDeviceToHost));
+      int64_t seen = 0;
+      for (auto v : hh) seen += v;
+      if (seen >= nq || lim >= h->hist_cap) break;
+      lim = std::min<int64_t>(h->hist_cap, lim * 16);
+    }
+    int64_t maxc = 0;
+    for (int64_t c = 0; c < (int64_t)hh.size(); c++)
+      if (hh[c]) maxc = c;
+    int64_t alive = nq;
+    for (int64_t i = 1; i <= maxc; i++) {
+      alive -= hh[i - 1];
+      h->active[d].push_back(alive);
+    }
+  }
+  m.iterations_left = (int64_t)h->active[0].size();
+  m.iterations_right = (int64_t)h->active[1].size();
+  m.distance_evals = (int64_t)cnt[0];
+  m.pruned_leaves = (int64_t)cnt[1];
+  m.pruning_violations = (int64_t)cnt[2];
+  m.clamped_objects = (int64_t)cnt[3];
+  m.n_results = total;
+  m.t_build_us = us_between(h->ev[0], h->ev[1]);
+  m.t_index_objects_us = us_between(h->ev[1], h->ev[2]);
+  m.t_index_queries_us = us_between(h->ev[2], h->ev[3]);
+  m.t_first_iteration_us = 0;  // fused into the search kernel (t_loop_us)
+  m.t_loop_us = us_between(h->ev[3], h->ev[4]);
+  m.t_emit_us = us_between(h->ev[4], h->ev[5]);
+
+  h->history.push_back(m.distance_evals);
+  h->tick += 1;
+  m.t_total_us = std::chrono::duration_cast<std::chrono::microseconds>(
+                     std::chrono::steady_clock::now() - t_start)
+                     .count();
+  if (met) *met = m;
+  return 0;
+}
+
+int validate_counts(mknn_engine* h, int64_t n, int64_t nq) {
+  if (n < 0 || nq < 0) return h->invalid("negative object or query count");
+  if (n > 0x7ffffff0LL) return h->invalid("more than 2^31 objects per tick");
+  if (nq > 0x7ffffff0LL) return h->invalid("more than 2^31 queries per tick");
+  if (nq * (int64_t)h->cfg.k > (int64_t)1 << 40) return h->invalid("result size too large");
+  return 0;
+}
+
+int check_unique_host(mknn_engine* h, int64_t n, const int64_t* ids) {
+  std::vector<int64_t> v(ids, ids + n);
+  std::sort(v.begin(), v.end());
+  if (std::adjacent_find(v.begin(), v.end()) != v.end())
+    return h->invalid("duplicate object ids in tick batch");  // engine.py:611-612
+  return 0;
+}
+
+int check_unique_dev(mknn_engine* h, int64_t n, const int64_t* d_ids) {
+  std::vector<int64_t> v((size_t)n);
+  if (n) MKNN_CUDA_OK(cudaMemcpy(v.data(), d_ids, sizeof(int64_t) * n, cudaMemcpyDeviceToHost));
+  return check_unique_host(h, n, v.data());
+}
+
+int ensure_out_dev(mknn_engine* h, int64_t nq) {
+  int rc;
+  const int64_t rows = std::max<int64_t>(nq * (int64_t)h->cfg.k, 1);
+  if (rows > h->cap_c) {
+    int64_t c = h->cap_c;
+    if ((rc = grow(h->c_nids, c, rows))) return rc;
+    c = h->cap_c;
+    if ((rc = grow(h->c_dist, c, rows))) return rc;
+    h->cap_c = c;
+  }
+  if ((rc = grow(h->offsets, h->cap_off, nq + 1))) return rc;
+  if ((rc = grow(h->out_qids, h->cap_oq, std::max<int64_t>(nq, 1)))) return rc;
+  if ((rc = grow(h->out_len, h->cap_len, std::max<int64_t>(nq, 1)))) return rc;
+  return 0;
+}
+
+// host-output tick over device-resident inputs (mknn_tick / mknn_query)
+int host_out_tick(mknn_engine* h, int64_t n, const long long* ids, const double* x, const double* y,
+                  int64_t nq, const long long* qi, const double* qx, const double* qy,
+                  int64_t* out_qids, int32_t* out_len, int64_t* out_nids, double* out_dist,
+                  mknn_metrics* metrics, std::chrono::steady_clock::time_point t0) {
+  int rc;
+  if ((rc = ensure_out_dev(h, nq))) return h->set_err(rc);
+  DevOut o{h->out_qids, h->out_len, h->offsets, h->c_nids, h->c_dist};
+  mknn_metrics m{};
+  if ((rc = core_tick(h, n, ids, x, y, nq, qi, qx, qy, o, &m, t0))) return rc;
+  cudaStream_t s = h->stream;
+  if (nq) {
+    MKNN_CUDA_OK(cudaMemcpyAsync(out_qids, h->out_qids, sizeof(int64_t) * nq, cudaMemcpyDeviceToHost, s));
+    MKNN_CUDA_OK(cudaMemcpyAsync(out_len, h->out_len, sizeof(int32_t) * nq, cudaMemcpyDeviceToHost, s));
+  }
+  if (m.n_results) {
+    MKNN_CUDA_OK(cudaMemcpyAsync(out_nids, h->c_nids, sizeof(int64_t) * m.n_results,
+                                 cudaMemcpyDeviceToHost, s));
+    MKNN_CUDA_OK(cudaMemcpyAsync(out_dist, h->c_dist, sizeof(double) * m.n_results,
+                                 cudaMemcpyDeviceToHost, s));
+  }
+  MKNN_CUDA_OK(cudaStreamSynchronize(s));
+  m.t_total_us = std::chrono::duration_cast<std::chrono::microseconds>(
+                     std::chrono::steady_clock::now() - t0)
+                     .count();
+  if (metrics) *metrics = m;
+  return 0;
+}
+
+int stage_queries(mknn_engine* h, int64_t nq, const int64_t* qi, const double* qx, const double* qy) {
+  int rc;
+  int64_t c = h->cap_qin;
+  if ((rc = grow(h->in_qi, c, std::max<int64_t>(nq, 1)))) return rc;
+  c = h->cap_qin;
+  if ((rc = grow(h->in_qx, c, std::max<int64_t>(nq, 1)))) return rc;
+  c = h->cap_qin;
+  if ((rc = grow(h->in_qy, c, std::max<int64_t>(nq, 1)))) return rc;
+  h->cap_qin = c;
+  cudaStream_t s = h->stream;
+  if (nq) {
+    MKNN_CUDA_OK(cudaMemcpyAsync(h->in_qi, qi, sizeof(int64_t) * nq, cudaMemcpyHostToDevice, s));
+    MKNN_CUDA_OK(cudaMemcpyAsync(h->in_qx, qx, sizeof(double) * nq, cudaMemcpyHostToDevice, s));
+    MKNN_CUDA_OK(cudaMemcpyAsync(h->in_qy, qy, sizeof(double) * nq, cudaMemcpyHostToDevice, s));
+  }
+  return 0;
+}
+
+// ----------------------------------------------------------- delta snapshot
+int snap_reserve(mknn_engine* h, int64_t want) {
+  if (want <= h->cap_snap && h->hkeys) return 0;
+  const int64_t nc = std::max<int64_t>(want, std::max<int64_t>(h->cap_snap * 3 / 2, 1024));
+  cudaStream_t s = h->stream;
+  long long* ni = nullptr;
+  double *nx = nullptr, *ny = nullptr;
+  MKNN_CUDA_OK(cudaMalloc(&ni, sizeof(long long) * nc));
+  MKNN_CUDA_OK(cudaMalloc(&nx, sizeof(double) * nc));
+  MKNN_CUDA_OK(cudaMalloc(&ny, sizeof(double) * nc));
+  if (h->n_snap) {
+    MKNN_CUDA_OK(cudaMemcpyAsync(ni, h->snap_ids, sizeof(long long) * h->n_snap, cudaMemcpyDeviceToDevice, s));
+    MKNN_CUDA_OK(cudaMemcpyAsync(nx, h->snap_x, sizeof(double) * h->n_snap, cudaMemcpyDeviceToDevice, s));
+    MKNN_CUDA_OK(cudaMemcpyAsync(ny, h->snap_y, sizeof(double) * h->n_snap, cudaMemcpyDeviceToDevice, s));
+  }
+  MKNN_CUDA_OK(cudaStreamSynchronize(s));
+  cudaFree(h->snap_ids);
+  cudaFree(h->snap_x);
+  cudaFree(h->snap_y);
+  h->snap_ids = ni;
+  h->snap_x = nx;
+  h->snap_y = ny;
+  h->cap_snap = nc;
+  // rehash at <= 50 % load
+  int64_t hc = 1;
+  while (hc < 2 * nc) hc <<= 1;
+  cudaFree(h->hkeys);
+  cudaFree(h->hvals);
+  cudaFree(h->winner);
+  MKNN_CUDA_OK(cudaMalloc(&h->hkeys, sizeof(long long) * hc));
+  MKNN_CUDA_OK(cudaMalloc(&h->hvals, sizeof(int32_t) * hc));
+  MKNN_CUDA_OK(cudaMalloc(&h->winner, sizeof(int32_t) * nc));
+  h->hcap = hc;
+  h->cap_winner = nc;
+  if (!h->d_nsnap) MKNN_CUDA_OK(cudaMalloc(&h->d_nsnap, sizeof(int32_t)));
+  k_fill_i64<<<gs_blocks(hc), 256, 0, s>>>(h->hkeys, hc, HASH_EMPTY);
+  k_fill_i32<<<gs_blocks(hc), 256, 0, s>>>(h->hvals, hc, -1);
+  k_fill_i32<<<gs_blocks(nc), 256, 0, s>>>(h->winner, nc, -1);
+  if (h->n_snap)
+    k_hash_load<<<gs_blocks(h->n_snap), 256, 0, s>>>(h->snap_ids, h->n_snap, h->hkeys, h->hvals,
+                                                       (uint64_t)(hc - 1), h->winner);
+  MKNN_CUDA_OK(cudaGetLastError());
+  return 0;
+}
+
+int snap_load_dev(mknn_engine* h, int64_t n, const long long* ids, const double* x, const double* y) {
+  int rc;
+  h->n_snap = 0;
+  if ((rc = snap_reserve(h, std::max<int64_t>(n, 1)))) return rc;
+  cudaStream_t s = h->stream;
+  if (n) {
+    MKNN_CUDA_OK(cudaMemcpyAsync(h->snap_ids, ids, sizeof(long long) * n, cudaMemcpyDeviceToDevice, s));
+    MKNN_CUDA_OK(cudaMemcpyAsync(h->snap_x, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    MKNN_CUDA_OK(cudaMemcpyAsync(h->snap_y, y, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  }
+  k_fill_i64<<<gs_blocks(h->hcap), 256, 0, s>>>(h->hkeys, h->hcap, HASH_EMPTY);
+  k_fill_i32<<<gs_blocks(h->hcap), 256, 0, s>>>(h->hvals, h->hcap, -1);
+  if (n)
+    k_hash_load<<<gs_blocks(n), 256, 0, s>>>(h->snap_ids, n, h->hkeys, h->hvals,
+                                               (uint64_t)(h->hcap - 1), h->winner);
+  MKNN_CUDA_OK(cudaGetLastError());
+  h->n_snap = n;
+  return 0;
+}
+
+int snap_update_dev(mknn_engine* h, int64_t nu, const long long* ids, const double* x, const double* y) {
+  int rc;
+  if (nu == 0) return 0;
+  if ((rc = snap_reserve(h, h->n_snap + nu))) return rc;
+  if ((rc = grow(h->slot_of, h->cap_slot_of, nu))) return rc;
+  cudaStream_t s = h->stream;
+  const int32_t ns = (int32_t)h->n_snap;
+  MKNN_CUDA_OK(cudaMemcpyAsync(h->d_nsnap, &ns, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  k_update_claim<<<gs_blocks(nu), 256, 0, s>>>(ids, nu, h->hkeys, h->hvals, (uint64_t)(h->hcap - 1),
+                                               h->d_nsnap, h->winner, h->slot_of);
+  k_update_apply<<<gs_blocks(nu), 256, 0, s>>>(ids, x, y, nu, h->slot_of, h->winner, h->snap_ids,
+                                               h->snap_x, h->snap_y);
+  k_update_reset<<<gs_blocks(nu), 256, 0, s>>>(nu, h->slot_of, h->winner);
+  MKNN_CUDA_OK(cudaGetLastError());
+  int32_t nn = 0;
+  MKNN_CUDA_OK(cudaMemcpyAsync(&nn, h->d_nsnap, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  MKNN_CUDA_OK(cudaStreamSynchronize(s));
+  h->n_snap = nn;
+  return 0;
+}
+
+}  // namespace
+
+// ===================================================================== ABI
+extern "C" {
+
+int mknn_abi_version(void) { return MKNN_ABI_VERSION; }
+
+int mknn_create(const mknn_config* cfg, mknn_engine** out) {
+  if (!cfg || !out) return MKNN_EINVAL;
+  *out = nullptr;
+  // EngineConfig.__post_init__ (engine.py:73-85) and build_index's checks
+  // (quadindex.py:86-89) -- the Python shim raises the same ValueErrors first.
+  if (cfg->k < 1 || cfg->th_quad < 1 || cfg->l_max < 1 || cfg->l_max > MAX_L_MAX ||
+      cfg->rebuild_window < 1 || !(cfg->rebuild_factor > 0))
+    return MKNN_EINVAL;
+  if (!(std::isfinite(cfg->x_lo) && std::isfinite(cfg->y_lo) && std::isfinite(cfg->x_hi) &&
+        std::isfinite(cfg->y_hi)) ||
+      cfg->x_lo > cfg->x_hi || cfg->y_lo > cfg->y_hi)
+    return MKNN_EINVAL;
+  if (cfg->k > 512) return MKNN_EUNSUPPORTED;
+  auto* h = new mknn_engine();
+  h->cfg = *cfg;
+  h->device = cfg->device;
+  h->r = Region{cfg->x_lo, cfg->y_lo, cfg->x_hi, cfg->y_hi, cfg->x_hi - cfg->x_lo, cfg->y_hi - cfg->y_lo};
+  int rc = bind(h);
+  if (!rc) rc = index_alloc(h->ix, cfg->l_max, cfg->th_quad);
+  if (!rc && cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking) != cudaSuccess) rc = E_CUDA;
+  for (int i = 0; i < 8 && !rc; i++)
+    if (cudaEventCreate(&h->ev[i]) != cudaSuccess) rc = E_CUDA;
+  if (rc) {
+    mknn_destroy(h);
+    return rc;
+  }
+  h->stream = h->own_stream;
+  *out = h;
+  return 0;
+}
+
+void mknn_destroy(mknn_engine* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  index_free(h->ix);
+  void* ptrs[] = {h->st.xy, h->st.ids, h->st.leaf, h->st.cell_count, h->st.cell_start, h->st.cell_fill,
+                  h->dq.leaf, h->dq.order, h->dq.qcount, h->dq.qstart, h->dq.qfill, h->dq.row,
+                  h->dq.keys, h->dq.keys_alt, h->dq.vals, h->dq.vals_alt, h->dq.minmax,
+                  h->in_ids, h->in_x, h->in_y, h->in_qi, h->in_qx, h->in_qy, h->out_len,
+                  h->out_nids, h->out_dist, h->c_nids, h->c_dist, h->offsets, h->out_qids,
+                  h->stats, h->counters, h->hist, h->snap_ids, h->snap_x, h->snap_y, h->hkeys,
+                  h->hvals, h->winner, h->slot_of, h->d_nsnap, h->up_ids, h->up_x, h->up_y};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  h->scratch.release();
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  delete h;
+}
+
+// the message of the most recent failure on the calling thread
+const char* mknn_last_error(const mknn_engine* h) {
+  (void)h;
+  return last_error_text();
+}
+
+int mknn_set_stream(mknn_engine* h, void* cuda_stream) {
+  if (!h) return MKNN_EINVAL;
+  h->stream = cuda_stream ? (cudaStream_t)cuda_stream : h->own_stream;
+  return 0;
+}
+
+int mknn_tick(mknn_engine* h, int64_t n, const int64_t* ids, const double* x, const double* y,
+              int64_t nq, const int64_t* q_issuer, const double* qx, const double* qy,
+              int64_t* out_qids, int32_t* out_len, int64_t* out_nids, double* out_dist,
+              mknn_metrics* metrics) {
+  if (!h) return MKNN_EINVAL;
+  const auto t0 = std::chrono::steady_clock::now();
+  int rc;
+  if ((rc = bind(h))) return h->set_err(rc);
+  if ((rc = validate_counts(h, n, nq))) return rc;
+  if ((n && (!ids || !x || !y)) || (nq && (!q_issuer || !qx || !qy || !out_qids || !out_len ||
+                                          !out_nids || !out_dist)))
+    return h->invalid("null buffer");
+  if (h->cfg.self_check && (rc = check_unique_host(h, n, ids))) return rc;
+  int64_t c = h->cap_in;
+  if ((rc = grow(h->in_ids, c, std::max<int64_t>(n, 1)))) return h->set_err(rc);
+  c = h->cap_in;
+  if ((rc = grow(h->in_x, c, std::max<int64_t>(n, 1)))) return h->set_err(rc);
+  c = h->cap_in;
+  if ((rc = grow(h->in_y, c, std::max<int64_t>(n, 1)))) return h->set_err(rc);
+  h->cap_in = c;
+  cudaStream_t s = h->stream;
+  if (n) {
+    MKNN_CUDA_OK(cudaMemcpyAsync(h->in_ids, ids, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+    MKNN_CUDA_OK(cudaMemcpyAsync(h->in_x, x, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    MKNN_CUDA_OK(cudaMemcpyAsync(h->in_y, y, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  }
+  if ((rc = stage_queries(h, nq, q_issuer, qx, qy))) return h->set_err(rc);
+  return host_out_tick(h, n, h->in_ids, h->in_x, h->in_y, nq, h->in_qi, h->in_qx, h->in_qy,
+                       out_qids, out_len, out_nids, out_dist, metrics, t0);
+}
+
+int mknn_tick_device(mknn_engine* h, int64_t n, const int64_t* d_ids, const double* d_x,
+                     const double* d_y, int64_t nq, const int64_t* d_q_issuer, const double* d_qx,
+                     const double* d_qy, int64_t* d_out_qids, int32_t* d_out_len,
+                     int64_t* d_out_offsets, int64_t* d_out_nids, double* d_out_dist,
+                     mknn_metrics* metrics) {
+  if (!h) return MKNN_EINVAL;
+  const auto t0 = std::chrono::steady_clock::now();
+  int rc;
+  if ((rc = bind(h))) return h->set_err(rc);
+  if ((rc = validate_counts(h, n, nq))) return rc;
+  if (!d_out_len || !d_out_offsets || (nq && (!d_out_nids || !d_out_dist)))
+    return h->invalid("null buffer");
+  if (h->cfg.self_check && (rc = check_unique_dev(h, n, d_ids))) return rc;
+  DevOut o{(long long*)d_out_qids, d_out_len, d_out_offsets, (long long*)d_out_nids, d_out_dist};
+  return core_tick(h, n, (const long long*)d_ids, d_x, d_y, nq, (const long long*)d_q_issuer, d_qx,
+                   d_qy, o, metrics, t0);
+}
+
+int mknn_load(mknn_engine* h, int64_t n, const int64_t* ids, const double* x, const double* y) {
+  if (!h) return MKNN_EINVAL;
+  int rc;
+  if ((rc = bind(h))) return h->set_err(rc);
+  if ((rc = validate_counts(h, n, 0))) return rc;
+  if (h->cfg.self_check && (rc = check_unique_host(h, n, ids))) return rc;
+  int64_t c = h->cap_up;
+  if ((rc = grow(h->up_ids, c, std::max<int64_t>(n, 1)))) return h->set_err(rc);
+  c = h->cap_up;
+  if ((rc = grow(h->up_x, c, std::max<int64_t>(n, 1)))) return h->set_err(rc);
+  c = h->cap_up;
+  if ((rc = grow(h->up_y, c, std::max<int64_t>(n, 1)))) return h->set_err(rc);
+  h->cap_up = c;
+  cudaStream_t s = h->stream;
+  if (n) {
+    MKNN_CUDA_OK(cudaMemcpyAsync(h->up_ids, ids, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+    MKNN_CUDA_OK(cudaMemcpyAsync(h->up_x, x, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    MKNN_CUDA_OK(cudaMemcpyAsync(h->up_y, y, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  }
+  if ((rc = snap_load_dev(h, n, h->up_ids, h->up_x, h->up_y))) return h->set_err(rc);
+  MKNN_CUDA_OK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int mknn_update_device(mknn_engine* h, int64_t nu, const int64_t* d_ids, const double* d_x,
+                       const double* d_y) {
+  if (!h) return MKNN_EINVAL;
+  int rc;
+  if ((rc = bind(h))) return h->set_err(rc);
+  if (nu < 0) return h->invalid("negative update count");
+  if (h->n_snap + nu > 0x7ffffff0LL) return h->invalid("snapshot larger than 2^31 objects");
+  if ((rc = snap_update_dev(h, nu, (const long long*)d_ids, d_x, d_y))) return h->set_err(rc);
+  return 0;
+}
+
+int mknn_update(mknn_engine* h, int64_t nu, const int64_t* ids, const double* x, const double* y) {
+  if (!h) return MKNN_EINVAL;
+  int rc;
+  if ((rc = bind(h))) return h->set_err(rc);
+  if (nu < 0) return h->invalid("negative update count");
+  if (nu == 0) return 0;
+  int64_t c = h->cap_up;
+  if ((rc = grow(h->up_ids, c, nu))) return h->set_err(rc);
+  c = h->cap_up;
+  if ((rc = grow(h->up_x, c, nu))) return h->set_err(rc);
+  c = h->cap_up;
+  if ((rc = grow(h->up_y, c, nu))) return h->set_err(rc);
+  h->cap_up = c;
+  cudaStream_t s = h->stream;
+  MKNN_CUDA_OK(cudaMemcpyAsync(h->up_ids, ids, sizeof(int64_t) * nu, cudaMemcpyHostToDevice, s));
+  MKNN_CUDA_OK(cudaMemcpyAsync(h->up_x, x, sizeof(double) * nu, cudaMemcpyHostToDevice, s));
+  MKNN_CUDA_OK(cudaMemcpyAsync(h->up_y, y, sizeof(double) * nu, cudaMemcpyHostToDevice, s));
+  return mknn_update_device(h, nu, (const int64_t*)h->up_ids, h->up_x, h->up_y);
+}
+
+int mknn_snapshot_size(const mknn_engine* h, int64_t* n) {
+  if (!h || !n) return MKNN_EINVAL;
+  *n = h->n_snap;
+  return 0;
+}
+
+int mknn_query(mknn_engine* h, int64_t nq, const int64_t* q_issuer, const double* qx,
+               const double* qy, int64_t* out_qids, int32_t* out_len, int64_t* out_nids,
+               double* out_dist, mknn_metrics* metrics) {
+  if (!h) return MKNN_EINVAL;
+  const auto t0 = std::chrono::steady_clock::now();
+  int rc;
+  if ((rc = bind(h))) return h->set_err(rc);
+  if ((rc = validate_counts(h, h->n_snap, nq))) return rc;
+  if (nq && (!q_issuer || !qx || !qy || !out_qids || !out_len || !out_nids || !out_dist))
+    return h->invalid("null buffer");
+  if ((rc = stage_queries(h, nq, q_issuer, qx, qy))) return h->set_err(rc);
+  return host_out_tick(h, h->n_snap, h->snap_ids, h->snap_x, h->snap_y, nq, h->in_qi, h->in_qx,
+                       h->in_qy, out_qids, out_len, out_nids, out_dist, metrics, t0);
+}
+
+int mknn_query_device(mknn_engine* h, int64_t nq, const int64_t* d_q_issuer, const double* d_qx,
+                      const double* d_qy, int64_t* d_out_qids, int32_t* d_out_len,
+                      int64_t* d_out_offsets, int64_t* d_out_nids, double* d_out_dist,
+                      mknn_metrics* metrics) {
+  if (!h) return MKNN_EINVAL;
+  const auto t0 = std::chrono::steady_clock::now();
+  int rc;
+  if ((rc = bind(h))) return h->set_err(rc);
+  if ((rc = validate_counts(h, h->n_snap, nq))) return rc;
+  DevOut o{(long long*)d_out_qids, d_out_len, d_out_offsets, (long long*)d_out_nids, d_out_dist};
+  return core_tick(h, h->n_snap, h->snap_ids, h->snap_x, h->snap_y, nq,
+                   (const long long*)d_q_issuer, d_qx, d_qy, o, metrics, t0);
+}
+
+int64_t mknn_active_counts(const mknn_engine* h, int dir, int64_t* out, int64_t cap) {
+  if (!h || dir < 0 || dir > 1) return MKNN_EINVAL;
+  const auto& v = h->active[dir];
+  for (int64_t i = 0; i < cap && i < (int64_t)v.size(); i++) out[i] = v[i];
+  return (int64_t)v.size();
+}
+
+int mknn_index_info(const mknn_engine* h, int32_t* l_deep, int64_t* n_leaves,
+                    int64_t* overfull_leaves, int64_t* n_build) {
+  if (!h) return MKNN_EINVAL;
+  if (!h->have_index) return MKNN_EINVAL;
+  if (l_deep) *l_deep = h->h_l_deep;
+  if (n_leaves) *n_leaves = h->h_n_leaves;
+  if (overfull_leaves) *overfull_leaves = h->h_overfull;
+  if (n_build) *n_build = h->h_n_build;
+  return 0;
+}
+
+int mknn_index_export(mknn_engine* h, int32_t* leaf_level, int64_t* leaf_code, int64_t* leaf_key,
+                      int64_t* leaf_span, int64_t* build_counts, int32_t* z_map) {
+  if (!h || !h->have_index) return MKNN_EINVAL;
+  int rc;
+  if ((rc = bind(h))) return h->set_err(rc);
+  const int64_t L = h->h_n_leaves;
+  std::vector<uint8_t> lv(L);
+  std::vector<uint32_t> lc(L), lk(L), ls(L);
+  std::vector<int32_t> bc(L);
+  MKNN_CUDA_OK(cudaStreamSynchronize(h->stream));
+  MKNN_CUDA_OK(cudaMemcpy(lv.data(), h->ix.leaf_level, L, cudaMemcpyDeviceToHost));
+  MKNN_CUDA_OK(cudaMemcpy(lc.data(), h->ix.leaf_code, 4 * L, cudaMemcpyDeviceToHost));
+  MKNN_CUDA_OK(cudaMemcpy(lk.data(), h->ix.leaf_key, 4 * L, cudaMemcpyDeviceToHost));
+  MKNN_CUDA_OK(cudaMemcpy(ls.data(), h->ix.leaf_span, 4 * L, cudaMemcpyDeviceToHost));
+  MKNN_CUDA_OK(cudaMemcpy(bc.data(), h->ix.build_counts, 4 * L, cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < L; i++) {
+    if (leaf_level) leaf_level[i] = lv[i];
+    if (leaf_code) leaf_code[i] = lc[i];
+    if (leaf_key) leaf_key[i] = lk[i];
+    if (leaf_span) leaf_span[i] = ls[i];
+    if (build_counts) build_counts[i] = bc[i];
+  }
+  if (z_map)
+    MKNN_CUDA_OK(cudaMemcpy(z_map, h->ix.z_map, sizeof(int32_t) * ((int64_t)1 << (2 * h->h_l_deep)),
+                            cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int mknn_store_export(mknn_engine* h, int64_t* cell_start, int64_t* cell_end) {
+  if (!h || !h->have_index || !h->st.cell_start) return MKNN_EINVAL;
+  int rc;
+  if ((rc = bind(h))) return h->set_err(rc);
+  const int64_t L = h->h_n_leaves;
+  std::vector<int32_t> cs(L + 1);
+  MKNN_CUDA_OK(cudaStreamSynchronize(h->stream));
+  MKNN_CUDA_OK(cudaMemcpy(cs.data(), h->st.cell_start, 4 * (L + 1), cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < L; i++) {
+    if (cell_start) cell_start[i] = cs[i];
+    if (cell_end) cell_end[i] = cs[i + 1];
+  }
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,151 @@
+// mknn_internal.h -- launchers shared between the translation units of
+// libmknn_b200.so.  Not part of the public C-ABI (see include/mknn_b200.h).
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "mknn_common.cuh"
+
+namespace mknn {
+
+int fail_cuda(cudaError_t e, const char* expr, const char* file, int line);
+int fail_msg(int code, const std::string& msg);
+const char* last_error_text();
+
+// error codes (C-ABI: 0 ok, < 0 error)
+constexpr int E_INVALID = -1;   // ValueError on the Python side
+constexpr int E_CUDA = -2;      // RuntimeError
+constexpr int E_UNSUPPORTED = -3;
+
+// ---------------------------------------------------------------- prims
+// Scratch sizing helpers: every primitive takes a caller-provided scratch
+// buffer of at least *_scratch_bytes(n) bytes.
+size_t scan_scratch_bytes(int64_t n);
+// exclusive scan of int32 counts -> int32 starts; also writes the total to
+// out[n] (so out has n + 1 entries).  n may be 0.
+int exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* scratch,
+                       cudaStream_t s);
+int exclusive_scan_i32_to_i64(const int32_t* in, int64_t* out, int64_t n, void* scratch,
+                              cudaStream_t s);
+
+// stable LSD radix sort of (key, value) pairs on the low `bits` bits of key
+size_t radix_scratch_bytes(int64_t n);
+int radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt,
+                         int64_t n, int bits, void* scratch, cudaStream_t s, bool* result_in_alt);
+
+// min / max of int64 keys into dev_out[2] (device memory)
+int minmax_i64(const int64_t* in, int64_t n, int64_t* dev_out, cudaStream_t s);
+
+// --------------------------------------------------------------- index
+struct DevIndex {
+  // pyramid of per-quadrant object counts at build time, levels 0..l_max
+  int32_t* counts = nullptr;   // concatenated, level l at pyramid_offset(l)
+  uint8_t* state = nullptr;    // same layout: 0 absent, 1 leaf, 2 split
+  int32_t* flags = nullptr;    // 4^l_max + 1 scan input / output
+  int32_t* z_map = nullptr;    // 4^l_max capacity, first 4^l_deep used
+  uint8_t* leaf_level = nullptr;
+  uint32_t* leaf_code = nullptr;
+  uint32_t* leaf_key = nullptr;
+  uint32_t* leaf_span = nullptr;
+  int32_t* build_counts = nullptr;
+  int32_t* scalars = nullptr;  // [0] l_deep, [1] n_leaves, [2] overfull, [3] n_build
+  int l_max = 0;
+  int th_quad = 0;
+};
+
+inline int64_t pyramid_offset(int level) { return pyramid_offset_dev(level); }
+inline int64_t pyramid_size(int l_max) { return pyramid_offset(l_max + 1); }
+
+int index_alloc(DevIndex& ix, int l_max, int th_quad);
+void index_free(DevIndex& ix);
+// quadindex.py:79-163 build_index on device from n positions
+int index_build(DevIndex& ix, const Region& r, const double* x, const double* y, int64_t n,
+                void* scratch, cudaStream_t s);
+
+// Per-tick object store (quadindex.py:166-213), leaf-sorted.
+struct DevStore {
+  double2* xy = nullptr;     // leaf-sorted positions
+  long long* ids = nullptr;  // leaf-sorted ids
+  uint32_t* leaf = nullptr;  // leaf ordinal per input object
+  int32_t* cell_count = nullptr;  // 4^l_max + 1
+  int32_t* cell_start = nullptr;  // 4^l_max + 2 (start[L] = n)
+  int32_t* cell_fill = nullptr;
+  int64_t cap = 0;
+};
+
+// quadindex.py:190-213 index_objects; clamped count accumulates into
+// dev_counters[0] (int64, device)
+int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const long long* ids,
+                        const double* x, const double* y, int64_t n, unsigned long long* dev_clamped,
+                        void* scratch, cudaStream_t s);
+
+// engine.py:201-217 index_queries (leaf ordinal + leaf-grouped order)
+struct DevQueries {
+  uint32_t* leaf = nullptr;     // own leaf per query (input order)
+  uint32_t* order = nullptr;    // queries grouped by leaf
+  int32_t* qcount = nullptr;    // per leaf
+  int32_t* qstart = nullptr;
+  int32_t* qfill = nullptr;
+  uint32_t* row = nullptr;      // emission row per query (stable issuer rank)
+  uint64_t* keys = nullptr;     // radix buffers
+  uint64_t* keys_alt = nullptr;
+  uint32_t* vals = nullptr;
+  uint32_t* vals_alt = nullptr;
+  int64_t* minmax = nullptr;    // device [2]
+  int64_t cap = 0;
+};
+
+int queries_index(DevQueries& dq, const DevIndex& ix, const Region& r, const long long* qi,
+                  const double* qx, const double* qy, int64_t nq, long long* out_qids,
+                  void* scratch, cudaStream_t s);
+
+// ------------------------------------------------------------- search
+struct QueryStats {
+  uint32_t evals;
+  uint32_t prunes;
+  uint16_t nav_left;
+  uint16_t nav_right;
+  uint32_t violations;
+};
+
+struct SearchArgs {
+  Region r;
+  int k;
+  int l_deep_host;  // -1: read from device scalars
+  const int32_t* scalars;
+  const int32_t* z_map;
+  const uint32_t* leaf_key;
+  const uint32_t* leaf_span;
+  const int32_t* cell_start;  // L + 1 entries
+  const double2* xy;
+  const long long* ids;
+  const uint32_t* q_order;
+  const uint32_t* q_leaf;
+  const uint32_t* q_row;
+  const long long* qi;
+  const double* qx;
+  const double* qy;
+  int64_t nq;
+  int32_t* out_len;       // [nq] by row
+  long long* out_nids;    // [nq * k] padded rows
+  double* out_dist;       // [nq * k]
+  QueryStats* stats;      // [nq] by leaf-grouped position
+  int audit;
+};
+
+int search_launch(const SearchArgs& a, cudaStream_t s);
+
+// reduce QueryStats into dev_tot (u64 [4]: evals, prunes, violations, unused)
+// and nav histograms (u32 [hist_cap] each) for active_left/right
+int stats_reduce(const QueryStats* st, int64_t nq, unsigned long long* dev_tot, uint32_t* hist_l,
+                 uint32_t* hist_r, int hist_cap, cudaStream_t s);
+
+// compact padded rows to CSR: offsets[nq + 1] (int64)
+int rows_compact(const int32_t* len, const long long* nids, const double* dist, int64_t nq, int k,
+                 int64_t* offsets, long long* c_nids, double* c_dist, void* scratch,
+                 cudaStream_t s);
+
+}  // namespace mknn

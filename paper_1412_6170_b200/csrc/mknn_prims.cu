@@ -1,0 +1,313 @@
+// mknn_prims.cu -- device-wide scan, stable LSD radix sort, min/max.
+//
+// Hand-written for sm_100a (no CUB/Thrust on the product path).  These back
+// the counting sorts of objects and queries by leaf (quadindex.py:197-202,
+// engine.py:208) and the stable issuer-order emission (engine.py:713,
+// oracle.py:56).
+#include <cstdio>
+#include <string>
+
+#include "mknn_internal.h"
+
+namespace mknn {
+
+static thread_local std::string g_err;
+
+int fail_cuda(cudaError_t e, const char* expr, const char* file, int line) {
+  char buf[512];
+  snprintf(buf, sizeof(buf), "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e),
+           cudaGetErrorString(e), file, line, expr);
+  g_err = buf;
+  return E_CUDA;
+}
+
+int fail_msg(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+const char* last_error_text() { return g_err.c_str(); }
+
+// ------------------------------------------------------------------ scan
+namespace {
+
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_ITEMS = 16;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;  // 4096
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T u = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v += u;
+  }
+  return v;
+}
+
+// exclusive block scan of one value per thread; returns the block total
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T* sh_warp, T& total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  T inc = warp_incl_scan(v);
+  if (lane == 31) sh_warp[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    T s = lane < nw ? sh_warp[lane] : T(0);
+    T si = warp_incl_scan(s);
+    if (lane < nw) sh_warp[lane] = si - s;
+    if (lane == nw - 1) sh_warp[32] = si;
+  }
+  __syncthreads();
+  total = sh_warp[32];
+  T r = inc - v + sh_warp[w];
+  __syncthreads();
+  return r;
+}
+
+__global__ void k_tile_sums(const int32_t* __restrict__ in, int64_t n, long long* sums) {
+  __shared__ long long sh[33];
+  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  long long acc = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    int64_t idx = base + (int64_t)i * SCAN_THREADS + threadIdx.x;
+    if (idx < n) acc += in[idx];
+  }
+  long long tot;
+  block_excl_scan<long long>(acc, sh, tot);
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void k_scan_sums(long long* sums, int64_t nb) {
+  __shared__ long long sh[33];
+  long long carry = 0;
+  for (int64_t base = 0; base < nb; base += blockDim.x) {
+    int64_t i = base + threadIdx.x;
+    long long v = i < nb ? sums[i] : 0;
+    long long tot;
+    long long ex = block_excl_scan<long long>(v, sh, tot);
+    if (i < nb) sums[i] = ex + carry;
+    carry += tot;
+  }
+}
+
+template <typename TO>
+__global__ void k_tile_apply(const int32_t* __restrict__ in, TO* __restrict__ out, int64_t n,
+                             const long long* __restrict__ sums) {
+  __shared__ long long sh[33];
+  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+  int32_t v[SCAN_ITEMS];
+  long long acc = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    int64_t idx = base + i;
+    v[i] = idx < n ? in[idx] : 0;
+    acc += v[i];
+  }
+  long long tot;
+  long long ex = block_excl_scan<long long>(acc, sh, tot) + sums[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    int64_t idx = base + i;
+    if (idx < n) out[idx] = (TO)ex;
+    ex += v[i];
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) out[n] = (TO)ex;
+}
+
+template <typename TO>
+__global__ void k_set_zero_total(TO* out) { out[0] = 0; }
+
+template <typename TO>
+int exclusive_scan_impl(const int32_t* in, TO* out, int64_t n, void* scratch, cudaStream_t s) {
+  if (n == 0) {
+    k_set_zero_total<TO><<<1, 1, 0, s>>>(out);
+    MKNN_CUDA_OK(cudaGetLastError());
+    return 0;
+  }
+  const int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+  long long* sums = (long long*)scratch;
+  k_tile_sums<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, n, sums);
+  k_scan_sums<<<1, 1024, 0, s>>>(sums, nb);
+  k_tile_apply<TO><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, out, n, sums);
+  MKNN_CUDA_OK(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace
+
+size_t scan_scratch_bytes(int64_t n) {
+  return sizeof(long long) * (size_t)((n + SCAN_TILE - 1) / SCAN_TILE + 1);
+}
+
+int exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* scratch,
+                       cudaStream_t s) {
+  return exclusive_scan_impl<int32_t>(in, out, n, scratch, s);
+}
+
+int exclusive_scan_i32_to_i64(const int32_t* in, int64_t* out, int64_t n, void* scratch,
+                              cudaStream_t s) {
+  return exclusive_scan_impl<int64_t>(in, out, n, scratch, s);
+}
+
+// ------------------------------------------------------------ radix sort
+namespace {
+
+constexpr int RX_THREADS = 256;
+constexpr int RX_WARPS = RX_THREADS / 32;
+constexpr int RX_ITEMS = 8;
+constexpr int RX_TILE = RX_THREADS * RX_ITEMS;  // 2048
+constexpr int RX_DIGITS = 256;
+
+__global__ void k_radix_hist(const uint64_t* __restrict__ keys, int64_t n, int shift,
+                             int32_t* __restrict__ hist, int64_t nb) {
+  __shared__ int32_t sh[RX_DIGITS];
+  sh[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * RX_TILE;
+#pragma unroll
+  for (int i = 0; i < RX_ITEMS; i++) {
+    int64_t idx = base + (int64_t)i * RX_THREADS + threadIdx.x;
+    if (idx < n) atomicAdd(&sh[(keys[idx] >> shift) & 0xFF], 1);
+  }
+  __syncthreads();
+  hist[(int64_t)threadIdx.x * nb + blockIdx.x] = sh[threadIdx.x];
+}
+
+// Stable scatter: warp w owns elements [tile + w*256, tile + (w+1)*256) and
+// walks them in 32-wide chunks, so (tile, warp, chunk, lane) is input order.
+__global__ void __launch_bounds__(RX_THREADS) k_radix_scatter(
+    const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+    uint64_t* __restrict__ okeys, uint32_t* __restrict__ ovals, int64_t n, int shift,
+    const int32_t* __restrict__ offs, int64_t nb) {
+  __shared__ uint32_t wcnt[RX_WARPS][RX_DIGITS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < RX_WARPS * RX_DIGITS; i += RX_THREADS) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t wbase = (int64_t)blockIdx.x * RX_TILE + (int64_t)w * 32 * RX_ITEMS;
+  const unsigned lt = (1u << lane) - 1u;
+  uint64_t k[RX_ITEMS];
+  uint32_t v[RX_ITEMS];
+  uint32_t rk[RX_ITEMS];
+  int dg[RX_ITEMS];
+#pragma unroll
+  for (int c = 0; c < RX_ITEMS; c++) {
+    const int64_t idx = wbase + c * 32 + lane;
+    const bool ok = idx < n;
+    k[c] = ok ? keys[idx] : 0;
+    v[c] = ok ? vals[idx] : 0;
+    const int d = (int)((k[c] >> shift) & 0xFF);
+    dg[c] = d;
+    unsigned eq = __ballot_sync(FULL, ok);
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+      const unsigned m = __ballot_sync(FULL, (d >> b) & 1);
+      eq &= ((d >> b) & 1) ? m : ~m;
+    }
+    uint32_t base = 0;
+    if (ok) base = wcnt[w][d];
+    __syncwarp();
+    const int cnt = __popc(eq);
+    const int r = __popc(eq & lt);
+    if (ok && r == cnt - 1) wcnt[w][d] = base + cnt;
+    __syncwarp();
+    rk[c] = base + r;
+  }
+  __syncthreads();
+  {
+    const int d = threadIdx.x;  // RX_THREADS == RX_DIGITS
+    uint32_t run = (uint32_t)offs[(int64_t)d * nb + blockIdx.x];
+#pragma unroll
+    for (int ww = 0; ww < RX_WARPS; ww++) {
+      const uint32_t t = wcnt[ww][d];
+      wcnt[ww][d] = run;
+      run += t;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < RX_ITEMS; c++) {
+    const int64_t idx = wbase + c * 32 + lane;
+    if (idx < n) {
+      const uint32_t pos = wcnt[w][dg[c]] + rk[c];
+      okeys[pos] = k[c];
+      ovals[pos] = v[c];
+    }
+  }
+}
+
+}  // namespace
+
+size_t radix_scratch_bytes(int64_t n) {
+  const int64_t nb = (n + RX_TILE - 1) / RX_TILE;
+  const int64_t hn = nb * RX_DIGITS;
+  return sizeof(int32_t) * (size_t)(2 * hn + 2) + scan_scratch_bytes(hn) + 256;
+}
+
+int radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt,
+                         int64_t n, int bits, void* scratch, cudaStream_t s,
+                         bool* result_in_alt) {
+  *result_in_alt = false;
+  if (n <= 1 || bits <= 0) return 0;
+  const int64_t nb = (n + RX_TILE - 1) / RX_TILE;
+  const int64_t hn = nb * RX_DIGITS;
+  int32_t* hist = (int32_t*)scratch;
+  int32_t* offs = hist + hn + 1;
+  void* sc = (void*)(((uintptr_t)(offs + hn + 1) + 255) & ~(uintptr_t)255);
+  uint64_t *ki = keys, *ko = keys_alt;
+  uint32_t *vi = vals, *vo = vals_alt;
+  for (int shift = 0; shift < bits; shift += 8) {
+    k_radix_hist<<<(unsigned)nb, RX_THREADS, 0, s>>>(ki, n, shift, hist, nb);
+    int rc = exclusive_scan_i32(hist, offs, hn, sc, s);
+    if (rc) return rc;
+    k_radix_scatter<<<(unsigned)nb, RX_THREADS, 0, s>>>(ki, vi, ko, vo, n, shift, offs, nb);
+    MKNN_CUDA_OK(cudaGetLastError());
+    std::swap(ki, ko);
+    std::swap(vi, vo);
+    *result_in_alt = !*result_in_alt;
+  }
+  return 0;
+}
+
+// --------------------------------------------------------------- minmax
+namespace {
+__global__ void k_minmax_init(int64_t* out) {
+  out[0] = 0x7fffffffffffffffLL;
+  out[1] = (int64_t)0x8000000000000000ULL;
+}
+__global__ void k_minmax(const int64_t* __restrict__ in, int64_t n, int64_t* out) {
+  long long lo = 0x7fffffffffffffffLL, hi = (long long)0x8000000000000000ULL;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    long long v = in[i];
+    lo = v < lo ? v : lo;
+    hi = v > hi ? v : hi;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    long long a = __shfl_xor_sync(FULL, lo, o), b = __shfl_xor_sync(FULL, hi, o);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin((long long*)&out[0], lo);
+    atomicMax((long long*)&out[1], hi);
+  }
+}
+}  // namespace
+
+int minmax_i64(const int64_t* in, int64_t n, int64_t* dev_out, cudaStream_t s) {
+  k_minmax_init<<<1, 1, 0, s>>>(dev_out);
+  if (n > 0) {
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    k_minmax<<<(unsigned)blocks, 256, 0, s>>>(in, n, dev_out);
+  }
+  MKNN_CUDA_OK(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace mknn

@@ -1,0 +1,209 @@
+"""GPU parity: the sm_100a path through the C-ABI against the reference's
+golden vectors and the pinned C oracle.
+
+Bar: neighbour ids and fp64 distances bit-identical to the reference oracle
+(brute_force_knn, oracle.py:41-106: canonical (d2, id) order); per-tick
+metrics (distance_evals, pruned_leaves, iterations, active counts, rebuild
+flags, clamped objects) identical to the reference engine on non-degenerate
+data; index arrays identical to build_index / index_objects.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from paper_1412_6170_b200 import Engine, EngineConfig, Rect, synth
+from tests import golden as G
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+CASES = G.case_names()
+DEGENERATE_TIES = {"hand_collinear_ties", "lattice_shuffled_ids_k8", "lattice_shuffled_ids_k32",
+                   "duplicate_coords_k17"}
+
+
+def assert_same(res, want):
+    np.testing.assert_array_equal(res.query_ids, want.query_ids)
+    np.testing.assert_array_equal(res.lengths, want.lengths)
+    np.testing.assert_array_equal(res.neighbour_ids, want.neighbour_ids)
+    assert res.distances.tobytes() == want.distances.tobytes()
+
+
+def engine_for(case):
+    m = case.meta
+    return Engine(EngineConfig(k=case.k, region=case.region, th_quad=case.th_quad,
+                               l_max=case.l_max, rebuild_window=m["rebuild_window"],
+                               rebuild_factor=m["rebuild_factor"]))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_golden_case(name):
+    case = G.load(name)
+    with engine_for(case) as eng:
+        for t, tick in enumerate(case.ticks):
+            res = eng.process_tick(tick.ids, tick.x, tick.y, tick.qi, tick.qx, tick.qy)
+            assert G.result_digest(res) == tick.meta["oracle_digest"], f"tick {t}"
+            if tick.has("o_nids"):
+                np.testing.assert_array_equal(res.neighbour_ids, tick["o_nids"])
+                assert res.distances.tobytes() == tick["o_dist"].tobytes()
+            m, want = eng.last_metrics, tick.meta["metrics"]
+            assert m.rebuild_flag == want["rebuild_flag"], f"tick {t}"
+            assert m.clamped_objects == want["clamped_objects"]
+            assert m.n_objects == want["n_objects"] and m.n_queries == want["n_queries"]
+            if name not in DEGENERATE_TIES:
+                for key in ("distance_evals", "pruned_leaves", "iterations_left",
+                            "iterations_right", "active_left", "active_right"):
+                    assert getattr(m, key) == want[key], (t, key, getattr(m, key), want[key])
+            ix = eng.index
+            wi = tick.meta["index"]
+            assert ix.l_deep == wi["l_deep"] and ix.n_leaves == wi["n_leaves"]
+            assert ix.overfull_leaves == wi["overfull_leaves"]
+            assert G.digest(ix.z_map.astype(np.int32)) == wi["z_map_digest"]
+            if tick.has("ix_leaf_level"):
+                for key in ("leaf_level", "leaf_code", "leaf_key", "leaf_span", "build_counts"):
+                    np.testing.assert_array_equal(getattr(ix, key), tick["ix_" + key], err_msg=key)
+                cs, ce = eng.cell_ranges()
+                np.testing.assert_array_equal(cs, tick["cell_start"])
+                np.testing.assert_array_equal(ce, tick["cell_end"])
+
+
+def test_cfg1_matches_reference():
+    """BASELINE.json configs[0]: uniform 100K, 10K queries, k=8."""
+    meta, arrs = G.load_cfg1()
+    snap = synth.place(100_000, "uniform", seed=0)
+    sel = np.random.default_rng(1).choice(100_000, 10_000, replace=False)
+    with Engine(EngineConfig(k=8, region=synth.REGION)) as eng:
+        res = eng.process_tick(snap.ids, snap.x, snap.y, snap.ids[sel], snap.x[sel], snap.y[sel])
+        m = eng.last_metrics
+        assert eng.index.n_leaves == meta["index"]["n_leaves"]
+    assert G.result_digest(res) == meta["oracle_digest"]
+    for key in ("distance_evals", "pruned_leaves", "iterations_left", "iterations_right",
+                "active_left", "active_right"):
+        assert getattr(m, key) == meta["metrics"][key], key
+
+
+@pytest.mark.parametrize("k", [1, 2, 5, 8, 16, 31, 32, 33, 64, 100, 128, 129, 200, 256, 300, 512])
+def test_random_vs_brute_force(k):
+    rng = np.random.default_rng(1000 + k)
+    n = int(rng.integers(500, 4000))
+    region = Rect.square(1000.0)
+    x = rng.uniform(0, 1000.0, n)
+    y = rng.uniform(0, 1000.0, n)
+    if k % 2:  # clustered + duplicated coordinates
+        x[: n // 4] = np.clip(rng.normal(300, 20, n // 4), 0, 1000)
+        y[: n // 4] = np.clip(rng.normal(700, 20, n // 4), 0, 1000)
+        x[n // 4: n // 4 + 50] = x[:50]
+        y[n // 4: n // 4 + 50] = y[:50]
+    ids = rng.permutation(n).astype(np.int64) * 5 - 777
+    nq = int(rng.integers(50, 600))
+    sel = rng.choice(n, nq, replace=False)
+    qi, qx, qy = ids[sel], x[sel].copy(), y[sel].copy()
+    qx[::7] = rng.uniform(0, 1000, qx[::7].size)  # queries away from their issuer
+    qi[::11] = 10 ** 12 + np.arange(qi[::11].size)  # issuers that are not objects
+    th = int(rng.choice([8, 32, 64, 128]))
+    with Engine(EngineConfig(k=k, region=region, th_quad=th, l_max=int(rng.integers(3, 11)))) as eng:
+        res = eng.process_tick(ids, x, y, qi, qx, qy)
+    assert_same(res, orc.brute_force_knn(ids, x, y, qi, qx, qy, k))
+
+
+def test_duplicate_issuers_keep_input_order():
+    rng = np.random.default_rng(5)
+    n = 800
+    x = rng.uniform(0, 100, n)
+    y = rng.uniform(0, 100, n)
+    ids = np.arange(n, dtype=np.int64)
+    qi = np.array([5, 3, 5, 9, 3, 5])
+    qx = rng.uniform(0, 100, 6)
+    qy = rng.uniform(0, 100, 6)
+    with Engine(EngineConfig(k=7, region=Rect.square(100.0), th_quad=16)) as eng:
+        res = eng.process_tick(ids, x, y, qi, qx, qy)
+    assert_same(res, orc.brute_force_knn(ids, x, y, qi, qx, qy, 7))
+
+
+def test_delta_path_equals_full_snapshot():
+    """load + update + query == process_tick on the carried-forward snapshot
+    (datasets.py:136-148)."""
+    snap = synth.place(30_000, "uniform", seed=11)
+    with Engine(EngineConfig(k=32, region=synth.REGION)) as full, \
+            Engine(EngineConfig(k=32, region=synth.REGION)) as delta:
+        delta.load(snap.ids, snap.x, snap.y)
+        for t in range(4):
+            if t:
+                uid, ux, uy = synth.updates(snap, 0.1, t, seed=11)
+                # duplicate updates inside a batch: the last one wins
+                uid = np.concatenate([uid[:100], uid])
+                ux = np.concatenate([ux[:100] + 1.0, ux])
+                uy = np.concatenate([uy[:100] + 1.0, uy])
+                delta.update(uid, ux, uy)
+                synth.apply_updates(snap, uid[100:], ux[100:], uy[100:])
+            qi, qx, qy = synth.queries(snap, 3000, seed=100 + t)
+            a = full.process_tick(snap.ids, snap.x, snap.y, qi, qx, qy)
+            b = delta.query(qi, qx, qy)
+            assert_same(b, a)
+            assert delta.last_metrics.distance_evals == full.last_metrics.distance_evals
+        # unseen ids are appended
+        delta.update(np.array([10 ** 9]), np.array([5.0]), np.array([5.0]))
+        assert delta.snapshot_size == 30_001
+
+
+def test_device_tensors_path():
+    snap = synth.place(50_000, "gaussian", seed=2, hotspots=4)
+    qi, qx, qy = synth.queries(snap, 5000, seed=2)
+    dev = torch.device("cuda:0")
+    T = lambda a: torch.as_tensor(a, device=dev)  # noqa: E731
+    with Engine(EngineConfig(k=16, region=synth.REGION)) as eng:
+        host = eng.process_tick(snap.ids, snap.x, snap.y, qi, qx, qy)
+        out = eng.tick_device(T(snap.ids), T(snap.x), T(snap.y), T(qi), T(qx), T(qy))
+        torch.cuda.synchronize()
+    nres = out["n_results"]
+    assert np.array_equal(out["query_ids"].cpu().numpy(), host.query_ids)
+    assert np.array_equal(out["lengths"].cpu().numpy(), host.lengths)
+    assert np.array_equal(out["offsets"].cpu().numpy(), host.offsets)
+    assert np.array_equal(out["neighbour_ids"][:nres].cpu().numpy(), host.neighbour_ids)
+    assert out["distances"][:nres].cpu().numpy().tobytes() == host.distances.tobytes()
+
+
+def test_audit_pruning_finds_no_violations():
+    snap = synth.place(20_000, "gaussian", seed=4, hotspots=5)
+    qi, qx, qy = synth.queries(snap, 2000, seed=4)
+    with Engine(EngineConfig(k=8, region=synth.REGION, th_quad=64, audit_pruning=True)) as eng:
+        eng.process_tick(snap.ids, snap.x, snap.y, qi, qx, qy)
+        m = eng.last_metrics
+    assert m.pruned_leaves > 0 and m.pruning_violations == 0
+
+
+def test_self_check_rejects_duplicate_ids():
+    with Engine(EngineConfig(k=1, region=Rect.square(10.0), th_quad=4, self_check=True)) as eng:
+        with pytest.raises(ValueError):
+            eng.process_tick(np.array([1, 1]), np.array([1.0, 2.0]), np.array([1.0, 2.0]),
+                             np.array([1]), np.array([1.0]), np.array([1.0]))
+
+
+def test_large_k_unsupported_is_loud():
+    with pytest.raises(NotImplementedError):
+        with Engine(EngineConfig(k=600, region=Rect.square(10.0))) as eng:
+            eng.process_tick(np.arange(3), np.ones(3), np.ones(3), [], [], [])
+
+
+@pytest.mark.parametrize("dist,n,nq,k,seed", [
+    ("gaussian", 1_000_000, 100_000, 32, 3),
+    ("uniform", 1_000_000, 100_000, 32, 0),
+])
+def test_large_vs_oracle_engine_port(dist, n, nq, k, seed):
+    """Full-size-class check: every query vs the pinned C port of the
+    reference engine (which is itself checked against the reference)."""
+    snap = synth.place(n, dist, seed=seed)
+    qi, qx, qy = synth.queries(snap, nq, seed=seed)
+    with Engine(EngineConfig(k=k, region=synth.REGION)) as eng:
+        res = eng.process_tick(snap.ids, snap.x, snap.y, qi, qx, qy)
+        m = eng.last_metrics
+    want = orc.engine_tick(snap.ids, snap.x, snap.y, qi, qx, qy, k, synth.REGION, 384)
+    assert_same(res, want)
+    assert m.distance_evals == want.metrics["distance_evals"]
+    assert m.pruned_leaves == want.metrics["pruned_leaves"]
+    assert m.active_left == want.metrics["active_left"]
+    assert m.active_right == want.metrics["active_right"]
