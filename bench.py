@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""Benchmark of the per-tick repeated k-NN join (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+                    [--workload cfg3|cfg3u|cfg2|cfg4|k1|k8|k32|k128]
+
+A step is one tick: a full position snapshot of n objects plus a batch of
+queries -> every query's k nearest (id, distance) lists, CSR in issuer order.
+Default workload (the metric is quoted "at 10M objects"): BASELINE.json
+configs[2], Gaussian-clustered n=10M (16 hotspots, sigma 500), 1M queries,
+k=32; synthetic data from the reference generator's placement draws
+(paper_1412_6170_b200/synth.py).
+
+* value: queries/s of the whole job with inputs resident in HBM
+  (Engine.tick_device: full snapshot + queries already on the device), timed
+  with CUDA events per step on the launching stream, L2 flushed between
+  steps outside the timed events, max over ranks.
+* e2e: the same metric through the reference-facing API (Engine.process_tick
+  -> C-ABI mknn_tick) with pinned HOST buffers: the H2D of the snapshot and
+  the queries and the D2H of the result CSR are inside every timed step.
+* roofline: the dominant kernel (k_search); algorithmic bytes per launch =
+  24*T + 24*Q + 16*Q*k (T = records the reference's distance tasks stream,
+  counted on device in one extra untimed instrumented step), divided by the
+  kernel's CUDA-event time (engine metrics t_loop_us).
+* cpu_baseline: the C port of the reference engine (oracle/, OpenMP, all host
+  threads) on a bounded sample, scaled to one tick.
+* --gpus N>1 (torchrun): weak scaling, each rank answers 1M queries of its
+  own against the replicated snapshot, whose 1/N slices are all-gathered
+  over NCCL every step (sharded.py).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "k-NN queries/sec per tick at 10M objects, 1/2/4/8 B200; % of HBM roofline"
+UNIT = "queries/s"
+
+WORKLOADS = {
+    "cfg3": dict(desc="Gaussian-clustered 10M objects (16 hotspots, sigma 500), 1M queries, k=32",
+                 dist="gaussian", n=10_000_000, nq=1_000_000, k=32, seed=3, baseline_idx=2),
+    "cfg3u": dict(desc="uniform 10M objects, 1M queries, k=32", dist="uniform", n=10_000_000,
+                  nq=1_000_000, k=32, seed=3, baseline_idx=2),
+    "cfg2": dict(desc="uniform 1M objects, 100K queries, k=32", dist="uniform", n=1_000_000,
+                 nq=100_000, k=32, seed=0, baseline_idx=1),
+    "cfg4": dict(desc="uniform 100M objects, 10M queries, k=16", dist="uniform", n=100_000_000,
+                 nq=10_000_000, k=16, seed=4, baseline_idx=3),
+}
+for _k in (1, 8, 32, 128):
+    WORKLOADS[f"k{_k}"] = dict(desc=f"Gaussian-clustered 10M objects, 1M queries, k={_k}",
+                               dist="gaussian", n=10_000_000, nq=1_000_000, k=_k, seed=3,
+                               baseline_idx=4)
+
+
+def load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """SM clocks and throttle reasons sampled through NVML every ~2 ms on a
+    background thread during the timed region (the timed region is only tens
+    of ms, shorter than nvidia-smi's sampling period)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self.max_mhz = None
+        self._stop = None
+
+    def _run(self, h, pynvml):
+        while not self._stop.is_set():
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, rs))
+            except Exception:
+                pass
+            self._stop.wait(0.002)
+
+    def __enter__(self):
+        import threading
+
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.gpu]) if vis else self.gpu
+            h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self._stop = threading.Event()
+            self._t = threading.Thread(target=self._run, args=(h, pynvml), daemon=True)
+            self._t.start()
+        except Exception:
+            self._stop = None
+        return self
+
+    def __exit__(self, *exc):
+        if self._stop is not None:
+            self._stop.set()
+            self._t.join(timeout=2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        reasons = sorted(nm for nm, bit in self.REASONS.items()
+                         if any(rs & bit for _, rs in self.samples))
+        return {"sm_mhz": statistics.median(sm for sm, _ in self.samples),
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_port_tick_seconds(snap, qi, qx, qy, k, region, th, sample_q):
+    """The C port of the reference engine (oracle/, test infrastructure used
+    here only as the reported CPU baseline): index-only tick + a query
+    sample, scaled to the full query count."""
+    from oracle import oracle as orc
+
+    t = time.perf_counter()
+    orc.engine_tick(snap.ids, snap.x, snap.y, qi[:0], qx[:0], qy[:0], k, region, th)
+    t_index = time.perf_counter() - t
+    t = time.perf_counter()
+    orc.engine_tick(snap.ids, snap.x, snap.y, qi[:sample_q], qx[:sample_q], qy[:sample_q], k,
+                    region, th)
+    t_sample = time.perf_counter() - t
+    per_q = max(t_sample - t_index, 0.0) / max(sample_q, 1)
+    return t_index + per_q * len(qi), t_index, t_sample, orc.num_threads()
+
+
+def make_inputs(wl, world=1, rank=0):
+    from paper_1412_6170_b200 import synth
+
+    snap = synth.place(wl["n"], wl["dist"], seed=wl["seed"])
+    nq_total = min(wl["nq"] * world, wl["n"])
+    qi, qx, qy = synth.queries(snap, nq_total, seed=wl["seed"])
+    if world > 1:
+        from paper_1412_6170_b200.sharded import shard_queries
+
+        sel = shard_queries(qi, world, rank)
+        qi, qx, qy = qi[sel], qx[sel], qy[sel]
+    return snap, qi, qx, qy
+
+
+def run_reference(args, wl):
+    """--impl reference: the reference's CPU algorithm (C port, all host
+    threads) on a bounded sample per step, scaled to one tick."""
+    from paper_1412_6170_b200 import synth
+    from paper_1412_6170_b200.engine import resolve_th_quad
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    snap, qi, qx, qy = make_inputs(wl)
+    th = resolve_th_quad("auto", wl["k"])
+    sample = min(len(qi), args.cpu_sample)
+    for _ in range(args.warmup):
+        cpu_port_tick_seconds(snap, qi, qx, qy, wl["k"], synth.REGION, th, min(sample, 1000))
+    secs = []
+    for _ in range(args.steps):
+        s, t_index, t_sample, threads = cpu_port_tick_seconds(snap, qi, qx, qy, wl["k"],
+                                                              synth.REGION, th, sample)
+        secs.append(s)
+    ms = 1e3 * statistics.mean(secs)
+    value = len(qi) / (ms / 1e3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl["desc"], "n_objects": wl["n"], "n_queries": len(qi),
+                   "k": wl["k"], "th_quad": th},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"full index over {wl['n']} objects + {sample} of {len(qi)} "
+                                   f"queries per step, scaled to the full query count "
+                                   f"(oracle/mknn_oracle.c, OpenMP)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
+    ap.add_argument("--cpu-sample", type=int, default=250_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1412_6170_b200 import Engine, EngineConfig, synth
+    from paper_1412_6170_b200 import _native
+    from paper_1412_6170_b200.engine import resolve_th_quad
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    k = wl["k"]
+    th = resolve_th_quad("auto", k)
+
+    snap, qi, qx, qy = make_inputs(wl, world, rank)
+    nq = len(qi)
+    lo, hi = (0, wl["n"])
+    if world > 1:
+        from paper_1412_6170_b200.sharded import ShardedEngine, shard_bounds
+
+        lo, hi = shard_bounds(wl["n"], world, rank)
+    T = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)  # noqa: E731
+    d_ids, d_x, d_y = T(snap.ids[lo:hi]), T(snap.x[lo:hi]), T(snap.y[lo:hi])
+    d_qi, d_qx, d_qy = T(qi), T(qx), T(qy)
+    cfg = EngineConfig(k=k, region=synth.REGION, device=local)
+    stream = torch.cuda.current_stream(dev)
+    if world > 1:
+        eng = ShardedEngine(cfg, local)
+        engine = eng.engine
+        step = lambda out: eng.tick_device(d_ids, d_x, d_y, d_qi, d_qx, d_qy, out=out)  # noqa: E731
+    else:
+        engine = Engine(cfg)
+        engine.set_stream(stream)
+        step = lambda out: engine.tick_device(d_ids, d_x, d_y, d_qi, d_qx, d_qy, out=out)  # noqa: E731
+    out = engine.alloc_device_out(nq, dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
+
+    for _ in range(args.warmup):
+        step(out)
+    torch.cuda.synchronize(dev)
+
+    # one extra untimed, instrumented step: T for the roofline
+    engine.instrument = True
+    step(out)
+    T_records = engine.last_streamed_records
+    engine.instrument = False
+    step(out)
+    torch.cuda.synchronize(dev)
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    search_us, tick_metrics = [], []
+    launches0 = _native.lib().mknn_kernel_launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush, outside the timed events
+            ev[i][0].record(stream)
+            step(out)
+            ev[i][1].record(stream)
+            m = engine.last_metrics
+            search_us.append(m.t_loop_us)
+            tick_metrics.append(m)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+    launches = _native.lib().mknn_kernel_launches() - launches0
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t_local = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t_local.item()) / args.steps
+    value = world * nq / (ms_per_step / 1e3)
+
+    # ---- e2e through the reference-facing API with pinned host buffers ----
+    e2e = None
+    if args.e2e_steps > 0:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+        if world == 1:
+            h_in = [pin(snap.ids), pin(snap.x), pin(snap.y), pin(qi), pin(qx), pin(qy)]
+            h_out = (torch.empty(nq, dtype=torch.int64).pin_memory().numpy(),
+                     torch.empty(nq, dtype=torch.int32).pin_memory().numpy(),
+                     torch.empty(nq * k, dtype=torch.int64).pin_memory().numpy(),
+                     torch.empty(nq * k, dtype=torch.float64).pin_memory().numpy())
+            engine.process_tick(*h_in, out=h_out)  # warm the host path
+            secs, nres = [], 0
+            for _ in range(args.e2e_steps):
+                t = time.perf_counter()
+                res = engine.process_tick(*h_in, out=h_out)
+                secs.append(time.perf_counter() - t)
+                nres = len(res.neighbour_ids)
+            h2d = 24 * wl["n"] + 24 * nq
+        else:
+            h_in = [pin(snap.ids[lo:hi]), pin(snap.x[lo:hi]), pin(snap.y[lo:hi]), pin(qi), pin(qx),
+                    pin(qy)]
+            eng.process_tick(*h_in)
+            secs, nres = [], 0
+            dist.barrier()
+            for _ in range(args.e2e_steps):
+                t = time.perf_counter()
+                res = eng.process_tick(*h_in)
+                secs.append(time.perf_counter() - t)
+                nres = len(res.neighbour_ids)
+            h2d = 24 * (hi - lo) + 24 * nq
+        t_e2e = torch.tensor([statistics.mean(secs)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * nq / float(t_e2e.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(12 * nq + 16 * nres)}
+
+    # ---- roofline of the dominant kernel (k_search) -----------------------
+    peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
+    peak = peaks.get("hbm_gbs")
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    if not peak:
+        peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    t_search_s = statistics.mean(search_us) / 1e6
+    search_bytes = 24 * T_records + 24 * nq + 16 * nq * k
+    achieved = search_bytes / t_search_s / 1e9
+    prof = load_json(os.path.join(ROOT, "profiles", "search_kernel_traffic.json")) or {}
+    traffic = prof.get("traffic_bytes_per_launch") if prof.get("workload") == args.workload else None
+    tick_bytes = 24 * wl["n"] + 64 * wl["n"] + 48 * nq + 24 * T_records + 16 * nq * k
+    m0 = tick_metrics[-1]
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {
+            "workload": wl["desc"], "baseline_config": wl["baseline_idx"], "n_objects": wl["n"],
+            "n_queries_per_gpu": nq, "k": k, "th_quad": th, "l_max": 10,
+            "parallelism": f"query shards x{world}, replicated index, NCCL all-gather of "
+                           f"snapshot slices" if world > 1 else "single GPU",
+            "l2": "flushed between steps (256 MB write outside the timed events); "
+                  "inputs 264 MB > 126 MB L2",
+            "timed": "Engine.tick_device per step: rebuild decision, index_objects, "
+                     "index_queries, search, emission to device CSR",
+        },
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "roofline": {
+            "bound": "hbm", "kernel": "k_search", "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "peak_source": peak_src,
+            "bytes_per_launch": int(search_bytes),
+            "bytes_formula": "24*T + 24*Q + 16*Q*k, T = streamed records counted on device",
+            "T": int(T_records), "t_launch_us": t_search_s * 1e6,
+            "tick_B_alg": int(tick_bytes),
+            "tick_frac": tick_bytes / (ms_per_step / 1e3) / 1e9 / peak,
+        },
+        "clocks": clk.summary(),
+        "tick_phases_us": {"build": m0.t_build_us, "index_objects": m0.t_index_objects_us,
+                           "index_queries": m0.t_index_queries_us, "search": m0.t_loop_us,
+                           "emit": m0.t_emit_us},
+        "tick_metrics": {"distance_evals": m0.distance_evals, "pruned_leaves": m0.pruned_leaves,
+                         "iterations_left": m0.iterations_left,
+                         "iterations_right": m0.iterations_right},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        s, t_index, t_sample, threads = cpu_port_tick_seconds(
+            snap, qi, qx, qy, k, synth.REGION, th, min(args.cpu_sample, nq))
+        line["cpu_baseline"] = {
+            "value": nq / s, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"C port of the reference engine (oracle/mknn_oracle.c): full index over "
+                      f"{wl['n']} objects ({t_index:.2f} s) + {min(args.cpu_sample, nq)} of {nq} "
+                      f"queries ({t_sample - t_index:.2f} s), scaled to {nq} queries"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        eng.close()
+        dist.destroy_process_group()
+    else:
+        engine.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -44,7 +44,7 @@ typedef struct mknn_config {
     int32_t self_check;
     int32_t audit_pruning;
     int32_t device; /* CUDA ordinal */
-    int32_t reserved;
+    int32_t instrument; /* bit 0: count streamed records T */
 } mknn_config;
 
 /* TickMetrics (engine.py:88-107).  Phase times are device times measured
@@ -69,6 +69,10 @@ typedef struct mknn_metrics {
     int64_t clamped_objects;
     int64_t n_results; /* sum of lengths (CSR size) */
     int64_t t_emit_us;
+    /* T: object records streamed by the reference's distance tasks = sum of
+     * leaf populations over distinct (iteration, direction, leaf) runs plus
+     * distinct own leaves; -1 unless config.instrument & 1 */
+    int64_t streamed_records;
 } mknn_metrics;
 
 /* Engine.__init__ + EngineConfig.__post_init__ (engine.py:561-568, 73-85). */
@@ -77,6 +81,8 @@ int mknn_create(const mknn_config* cfg, mknn_engine** out);
 void mknn_destroy(mknn_engine* h);
 const char* mknn_last_error(const mknn_engine* h);
 int mknn_abi_version(void);
+/* Cumulative number of kernels this library has launched (process-wide). */
+int64_t mknn_kernel_launches(void);
 
 /* Run the engine's work on this cudaStream_t (NULL = the engine's own). */
 int mknn_set_stream(mknn_engine* h, void* cuda_stream);
@@ -120,6 +126,14 @@ int mknn_query_device(mknn_engine* h, int64_t nq, const int64_t* d_q_issuer, con
                       const double* d_qy, int64_t* d_out_qids, int32_t* d_out_len,
                       int64_t* d_out_offsets, int64_t* d_out_nids, double* d_out_dist,
                       mknn_metrics* metrics);
+
+/* Toggle instrumentation (mknn_config.instrument bits) between ticks. */
+int mknn_set_instrument(mknn_engine* h, int32_t flags);
+
+/* Multi-GPU: replace the last tick's entry of the rebuild history
+ * (quadindex.py:231-246 input, engine.py:692) with the job-wide
+ * distance_evals, so every rank takes the same rebuild decisions. */
+int mknn_set_last_evals(mknn_engine* h, int64_t distance_evals);
 
 /* TickMetrics.active_left / active_right of the last tick (engine.py:661-663):
  * dir 0 = left, 1 = right.  Writes min(cap, len) entries, returns len. */

@@ -396,7 +396,29 @@ typedef struct {
     int64_t clamped_objects;
     int64_t iterations_left;
     int64_t iterations_right;
+    int64_t streamed_records; /* T: sum of populations over distinct runs */
 } or_metrics;
+
+/* growable per-thread buffer of distance-task keys (dir, iteration, leaf) */
+typedef struct {
+    uint64_t *k;
+    int64_t n, cap;
+} keybuf;
+
+static inline void kb_push(keybuf *b, uint64_t key) {
+    if (b->n == b->cap) {
+        b->cap = b->cap ? 2 * b->cap : 1024;
+        b->k = (uint64_t *)realloc(b->k, sizeof(uint64_t) * b->cap);
+    }
+    b->k[b->n++] = key;
+}
+
+static int cmp_u64(const void *a, const void *b) {
+    uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+    return x < y ? -1 : x > y;
+}
+
+#define TASK_KEY(dir, it, leaf) (((uint64_t)(dir) << 60) | ((uint64_t)(it) << 40) | (uint64_t)(leaf))
 
 typedef struct {
     const or_index *ix;
@@ -506,9 +528,19 @@ OR_EXPORT int or_engine_tick(int64_t n, const int64_t *ids, const double *x, con
 
     int64_t evals = 0, pruned = 0;
     int32_t maxl = 0, maxr = 0;
+    int nthr = 1;
+#ifdef _OPENMP
+    nthr = omp_get_max_threads();
+#endif
+    keybuf *kbs = (keybuf *)calloc((size_t)nthr, sizeof(keybuf));
 #pragma omp parallel reduction(+ : evals, pruned) reduction(max : maxl, maxr)
     {
         cand_t *Lst = (cand_t *)malloc(sizeof(cand_t) * (size_t)k);
+        int tid = 0;
+#ifdef _OPENMP
+        tid = omp_get_thread_num();
+#endif
+        keybuf *kb = &kbs[tid];
 #pragma omp for schedule(dynamic, 64)
         for (int64_t t = 0; t < nq; t++) {
             int64_t q = qperm[t];
@@ -517,7 +549,10 @@ OR_EXPORT int or_engine_tick(int64_t n, const int64_t *ids, const double *x, con
             int64_t own = qleaf[q];
             int cnt = 0;
             /* engine.py:356-373 first_iteration (rows with 0 candidates dropped) */
-            if (ce[own] > cs[own]) evals += merge_leaf(&c, own, ax, ay, me, Lst, k, &cnt);
+            if (ce[own] > cs[own]) {
+                evals += merge_leaf(&c, own, ax, ay, me, Lst, k, &cnt);
+                kb_push(kb, TASK_KEY(0, 0, own));
+            }
             /* engine.py:645-681 direction loop, left first */
             int64_t cur[2] = {ix->leaf_key[own] - 1, ix->leaf_key[own] + ix->leaf_span[own]};
             int active[2] = {1, 1};
@@ -529,8 +564,12 @@ OR_EXPORT int or_engine_tick(int64_t n, const int64_t *ids, const double *x, con
                     int64_t pr = 0;
                     int64_t li = navigate_one(&c, d ? 1 : -1, &cur[d], ax, ay, Lst, k, cnt, &pr);
                     pruned += pr;
-                    if (li < 0) active[d] = 0;
-                    else evals += merge_leaf(&c, li, ax, ay, me, Lst, k, &cnt);
+                    if (li < 0) {
+                        active[d] = 0;
+                    } else {
+                        evals += merge_leaf(&c, li, ax, ay, me, Lst, k, &cnt);
+                        kb_push(kb, TASK_KEY(d + 1, calls[d] - 1, li));
+                    }
                 }
                 d ^= 1;
             }
@@ -549,6 +588,27 @@ OR_EXPORT int or_engine_tick(int64_t n, const int64_t *ids, const double *x, con
         }
         free(Lst);
     }
+    /* T: each reference run is one distinct
+     * (direction, iteration, leaf); its population is streamed once */
+    int64_t nk = 0;
+    for (int t = 0; t < nthr; t++) nk += kbs[t].n;
+    uint64_t *all = (uint64_t *)malloc(sizeof(uint64_t) * (nk ? nk : 1));
+    int64_t w = 0;
+    for (int t = 0; t < nthr; t++) {
+        memcpy(all + w, kbs[t].k, sizeof(uint64_t) * kbs[t].n);
+        w += kbs[t].n;
+        free(kbs[t].k);
+    }
+    free(kbs);
+    qsort(all, (size_t)nk, sizeof(uint64_t), cmp_u64);
+    int64_t T = 0;
+    for (int64_t i = 0; i < nk; i++) {
+        if (i && all[i] == all[i - 1]) continue;
+        int64_t leaf = (int64_t)(all[i] & ((1ull << 40) - 1));
+        T += ce[leaf] - cs[leaf];
+    }
+    free(all);
+    met->streamed_records = T;
     met->distance_evals = evals;
     met->pruned_leaves = pruned;
     met->iterations_left = maxl;

@@ -42,7 +42,7 @@ class _Index(ctypes.Structure):
 class _Metrics(ctypes.Structure):
     _fields_ = [("distance_evals", ctypes.c_int64), ("pruned_leaves", ctypes.c_int64),
                 ("clamped_objects", ctypes.c_int64), ("iterations_left", ctypes.c_int64),
-                ("iterations_right", ctypes.c_int64)]
+                ("iterations_right", ctypes.c_int64), ("streamed_records", ctypes.c_int64)]
 
 
 def build() -> str:
@@ -219,6 +219,7 @@ def engine_tick(ids, x, y, q_issuer, qx, qy, k: int, region, th_quad: int,
         distance_evals=int(met.distance_evals), pruned_leaves=int(met.pruned_leaves),
         clamped_objects=int(met.clamped_objects), iterations_left=int(met.iterations_left),
         iterations_right=int(met.iterations_right),
+        streamed_records=int(met.streamed_records),
         active_left=active_counts(navl), active_right=active_counts(navr),
         l_deep=int(l_deep.value), n_leaves=int(n_leaves.value))
     return res

@@ -29,7 +29,7 @@ class Config(ctypes.Structure):
         ("x_lo", ctypes.c_double), ("y_lo", ctypes.c_double), ("x_hi", ctypes.c_double),
         ("y_hi", ctypes.c_double), ("self_check", ctypes.c_int32),
         ("audit_pruning", ctypes.c_int32), ("device", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("instrument", ctypes.c_int32),
     ]
 
 
@@ -37,7 +37,7 @@ METRIC_FIELDS = (
     "tick", "n_objects", "n_queries", "iterations_left", "iterations_right", "distance_evals",
     "pruned_leaves", "rebuild_flag", "t_build_us", "t_index_objects_us", "t_index_queries_us",
     "t_first_iteration_us", "t_loop_us", "t_total_us", "pruning_violations", "clamped_objects",
-    "n_results", "t_emit_us",
+    "n_results", "t_emit_us", "streamed_records",
 )
 
 
@@ -48,6 +48,7 @@ class Metrics(ctypes.Structure):
 # name -> (restype, argtypes); every symbol include/mknn_b200.h declares
 SIGNATURES = {
     "mknn_abi_version": (ctypes.c_int, []),
+    "mknn_kernel_launches": (ctypes.c_int64, []),
     "mknn_create": (ctypes.c_int, [ctypes.POINTER(Config), ctypes.POINTER(_vp)]),
     "mknn_destroy": (None, [_vp]),
     "mknn_last_error": (ctypes.c_char_p, [_vp]),
@@ -65,6 +66,8 @@ SIGNATURES = {
                                   ctypes.POINTER(Metrics)]),
     "mknn_query_device": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                          _vp, ctypes.POINTER(Metrics)]),
+    "mknn_set_instrument": (ctypes.c_int, [_vp, ctypes.c_int32]),
+    "mknn_set_last_evals": (ctypes.c_int, [_vp, ctypes.c_int64]),
     "mknn_active_counts": (ctypes.c_int64, [_vp, ctypes.c_int, _i64p, ctypes.c_int64]),
     "mknn_index_info": (ctypes.c_int, [_vp, _i32p, _i64p, _i64p, _i64p]),
     "mknn_index_export": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -183,6 +184,10 @@ struct mknn_engine {
   QueryStats* stats = nullptr; int64_t cap_stats = 0;
   unsigned long long* counters = nullptr;  // [0] evals [1] prunes [2] viol [3] clamped
   uint32_t* hist = nullptr;                // 2 x hist_cap
+  // instrumentation buffers (config.instrument & 1)
+  unsigned long long *tk = nullptr, *tk_alt = nullptr, *tk_cnt = nullptr;
+  uint32_t *tv = nullptr, *tv_alt = nullptr;
+  int64_t cap_tk = 0;
   int hist_cap = 0;
   Buf scratch;
 
@@ -365,8 +370,49 @@ int core_tick(mknn_engine* h, int64_t n, const long long* ids, const double* x, 
   a.out_dist = h->out_dist;
   a.stats = h->stats;
   a.audit = h->cfg.audit_pruning;
+  {
+    static const char* tp = getenv("MKNN_TPQ");
+    static const char* dp = getenv("MKNN_DEBUG_PHASE");
+    a.force_warp = !(tp && tp[0] == '1');
+    a.debug_phase = dp ? atoi(dp) : 0;
+  }
+  const bool instr = (h->cfg.instrument & 1) != 0;
+  if (instr) {
+    const int64_t want = std::max<int64_t>(16 * nq, 1024);
+    if (want > h->cap_tk) {
+      cudaFree(h->tk); cudaFree(h->tk_alt); cudaFree(h->tv); cudaFree(h->tv_alt);
+      h->tk = h->tk_alt = nullptr; h->tv = h->tv_alt = nullptr; h->cap_tk = 0;
+      MKNN_CUDA_OK(cudaMalloc(&h->tk, 8 * want));
+      MKNN_CUDA_OK(cudaMalloc(&h->tk_alt, 8 * want));
+      MKNN_CUDA_OK(cudaMalloc(&h->tv, 4 * want));
+      MKNN_CUDA_OK(cudaMalloc(&h->tv_alt, 4 * want));
+      if (!h->tk_cnt) MKNN_CUDA_OK(cudaMalloc(&h->tk_cnt, 16));
+      h->cap_tk = want;
+    }
+    MKNN_CUDA_OK(cudaMemsetAsync(h->tk_cnt, 0, 16, s));
+    a.task_keys = h->tk;
+    a.task_count = h->tk_cnt;
+    a.task_cap = h->cap_tk;
+  }
   if ((rc = search_launch(a, s))) return h->set_err(rc);
   MKNN_CUDA_OK(cudaEventRecord(h->ev[4], s));
+  m.streamed_records = -1;
+  if (instr) {
+    unsigned long long nk = 0;
+    MKNN_CUDA_OK(cudaMemcpyAsync(&nk, h->tk_cnt, 8, cudaMemcpyDeviceToHost, s));
+    MKNN_CUDA_OK(cudaStreamSynchronize(s));
+    if ((int64_t)nk <= h->cap_tk) {
+      size_t need = radix_scratch_bytes((int64_t)nk) + 1024;
+      if ((rc = h->scratch.ensure(std::max(need, h->scratch.cap)))) return h->set_err(rc);
+      if ((rc = streamed_records(h->tk, h->tk_alt, h->tv, h->tv_alt, (int64_t)nk, h->st.cell_start,
+                                 h->tk_cnt + 1, h->scratch.p, s)))
+        return h->set_err(rc);
+      unsigned long long T = 0;
+      MKNN_CUDA_OK(cudaMemcpyAsync(&T, h->tk_cnt + 1, 8, cudaMemcpyDeviceToHost, s));
+      MKNN_CUDA_OK(cudaStreamSynchronize(s));
+      m.streamed_records = (int64_t)T;
+    }
+  }
   MKNN_CUDA_OK(cudaMemsetAsync(h->hist, 0, sizeof(uint32_t) * 2 * h->hist_cap, s));
   if ((rc = stats_reduce(h->stats, nq, h->counters, h->hist, h->hist + h->hist_cap, h->hist_cap, s)))
     return h->set_err(rc);
@@ -552,11 +598,11 @@ int snap_reserve(mknn_engine* h, int64_t want) {
   h->hcap = hc;
   h->cap_winner = nc;
   if (!h->d_nsnap) MKNN_CUDA_OK(cudaMalloc(&h->d_nsnap, sizeof(int32_t)));
-  k_fill_i64<<<gs_blocks(hc), 256, 0, s>>>(h->hkeys, hc, HASH_EMPTY);
-  k_fill_i32<<<gs_blocks(hc), 256, 0, s>>>(h->hvals, hc, -1);
-  k_fill_i32<<<gs_blocks(nc), 256, 0, s>>>(h->winner, nc, -1);
+  MKNN_LAUNCH k_fill_i64<<<gs_blocks(hc), 256, 0, s>>>(h->hkeys, hc, HASH_EMPTY);
+  MKNN_LAUNCH k_fill_i32<<<gs_blocks(hc), 256, 0, s>>>(h->hvals, hc, -1);
+  MKNN_LAUNCH k_fill_i32<<<gs_blocks(nc), 256, 0, s>>>(h->winner, nc, -1);
   if (h->n_snap)
-    k_hash_load<<<gs_blocks(h->n_snap), 256, 0, s>>>(h->snap_ids, h->n_snap, h->hkeys, h->hvals,
+    MKNN_LAUNCH k_hash_load<<<gs_blocks(h->n_snap), 256, 0, s>>>(h->snap_ids, h->n_snap, h->hkeys, h->hvals,
                                                        (uint64_t)(hc - 1), h->winner);
   MKNN_CUDA_OK(cudaGetLastError());
   return 0;
@@ -572,10 +618,10 @@ int snap_load_dev(mknn_engine* h, int64_t n, const long long* ids, const double*
     MKNN_CUDA_OK(cudaMemcpyAsync(h->snap_x, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     MKNN_CUDA_OK(cudaMemcpyAsync(h->snap_y, y, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   }
-  k_fill_i64<<<gs_blocks(h->hcap), 256, 0, s>>>(h->hkeys, h->hcap, HASH_EMPTY);
-  k_fill_i32<<<gs_blocks(h->hcap), 256, 0, s>>>(h->hvals, h->hcap, -1);
+  MKNN_LAUNCH k_fill_i64<<<gs_blocks(h->hcap), 256, 0, s>>>(h->hkeys, h->hcap, HASH_EMPTY);
+  MKNN_LAUNCH k_fill_i32<<<gs_blocks(h->hcap), 256, 0, s>>>(h->hvals, h->hcap, -1);
   if (n)
-    k_hash_load<<<gs_blocks(n), 256, 0, s>>>(h->snap_ids, n, h->hkeys, h->hvals,
+    MKNN_LAUNCH k_hash_load<<<gs_blocks(n), 256, 0, s>>>(h->snap_ids, n, h->hkeys, h->hvals,
                                                (uint64_t)(h->hcap - 1), h->winner);
   MKNN_CUDA_OK(cudaGetLastError());
   h->n_snap = n;
@@ -590,11 +636,11 @@ int snap_update_dev(mknn_engine* h, int64_t nu, const long long* ids, const doub
   cudaStream_t s = h->stream;
   const int32_t ns = (int32_t)h->n_snap;
   MKNN_CUDA_OK(cudaMemcpyAsync(h->d_nsnap, &ns, sizeof(int32_t), cudaMemcpyHostToDevice, s));
-  k_update_claim<<<gs_blocks(nu), 256, 0, s>>>(ids, nu, h->hkeys, h->hvals, (uint64_t)(h->hcap - 1),
+  MKNN_LAUNCH k_update_claim<<<gs_blocks(nu), 256, 0, s>>>(ids, nu, h->hkeys, h->hvals, (uint64_t)(h->hcap - 1),
                                                h->d_nsnap, h->winner, h->slot_of);
-  k_update_apply<<<gs_blocks(nu), 256, 0, s>>>(ids, x, y, nu, h->slot_of, h->winner, h->snap_ids,
+  MKNN_LAUNCH k_update_apply<<<gs_blocks(nu), 256, 0, s>>>(ids, x, y, nu, h->slot_of, h->winner, h->snap_ids,
                                                h->snap_x, h->snap_y);
-  k_update_reset<<<gs_blocks(nu), 256, 0, s>>>(nu, h->slot_of, h->winner);
+  MKNN_LAUNCH k_update_reset<<<gs_blocks(nu), 256, 0, s>>>(nu, h->slot_of, h->winner);
   MKNN_CUDA_OK(cudaGetLastError());
   int32_t nn = 0;
   MKNN_CUDA_OK(cudaMemcpyAsync(&nn, h->d_nsnap, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
@@ -609,6 +655,8 @@ int snap_update_dev(mknn_engine* h, int64_t nu, const long long* ids, const doub
 extern "C" {
 
 int mknn_abi_version(void) { return MKNN_ABI_VERSION; }
+
+int64_t mknn_kernel_launches(void) { return (int64_t)launch_count(); }
 
 int mknn_create(const mknn_config* cfg, mknn_engine** out) {
   if (!cfg || !out) return MKNN_EINVAL;
@@ -652,7 +700,8 @@ void mknn_destroy(mknn_engine* h) {
                   h->in_ids, h->in_x, h->in_y, h->in_qi, h->in_qx, h->in_qy, h->out_len,
                   h->out_nids, h->out_dist, h->c_nids, h->c_dist, h->offsets, h->out_qids,
                   h->stats, h->counters, h->hist, h->snap_ids, h->snap_x, h->snap_y, h->hkeys,
-                  h->hvals, h->winner, h->slot_of, h->d_nsnap, h->up_ids, h->up_x, h->up_y};
+                  h->hvals, h->winner, h->slot_of, h->d_nsnap, h->up_ids, h->up_x, h->up_y,
+                  h->tk, h->tk_alt, h->tk_cnt, h->tv, h->tv_alt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   h->scratch.release();
@@ -811,6 +860,18 @@ int mknn_query_device(mknn_engine* h, int64_t nq, const int64_t* d_q_issuer, con
   DevOut o{(long long*)d_out_qids, d_out_len, d_out_offsets, (long long*)d_out_nids, d_out_dist};
   return core_tick(h, h->n_snap, h->snap_ids, h->snap_x, h->snap_y, nq,
                    (const long long*)d_q_issuer, d_qx, d_qy, o, metrics, t0);
+}
+
+int mknn_set_instrument(mknn_engine* h, int32_t flags) {
+  if (!h) return MKNN_EINVAL;
+  h->cfg.instrument = flags;
+  return 0;
+}
+
+int mknn_set_last_evals(mknn_engine* h, int64_t distance_evals) {
+  if (!h || h->history.empty() || distance_evals < 0) return MKNN_EINVAL;
+  h->history.back() = distance_evals;
+  return 0;
 }
 
 int64_t mknn_active_counts(const mknn_engine* h, int dir, int64_t* out, int64_t cap) {

@@ -238,24 +238,24 @@ int index_build(DevIndex& ix, const Region& r, const double* x, const double* y,
   uint8_t* cell_lvl = reinterpret_cast<uint8_t*>(ix.flags + 2 * ncap + 2);
   MKNN_CUDA_OK(cudaMemsetAsync(ix.scalars, 0, sizeof(int32_t) * 8, s));
   MKNN_CUDA_OK(cudaMemsetAsync(ix.counts + pyramid_offset(L), 0, sizeof(int32_t) * ncap, s));
-  if (n > 0) k_hist_lmax<<<grid_stride_blocks(n), TPB, 0, s>>>(x, y, n, r, L, ix.counts + pyramid_offset(L));
+  if (n > 0) MKNN_LAUNCH k_hist_lmax<<<grid_stride_blocks(n), TPB, 0, s>>>(x, y, n, r, L, ix.counts + pyramid_offset(L));
   for (int l = L - 1; l >= 0; l--) {
     const int64_t np = int64_t(1) << (2 * l);
-    k_pyramid<<<blocks_for(np), TPB, 0, s>>>(ix.counts + pyramid_offset(l),
+    MKNN_LAUNCH k_pyramid<<<blocks_for(np), TPB, 0, s>>>(ix.counts + pyramid_offset(l),
                                               ix.counts + pyramid_offset(l + 1), np);
   }
   for (int l = 0; l <= L; l++) {
     const int64_t nc = int64_t(1) << (2 * l);
-    k_classify<<<blocks_for(nc), TPB, 0, s>>>(ix.counts + pyramid_offset(l),
+    MKNN_LAUNCH k_classify<<<blocks_for(nc), TPB, 0, s>>>(ix.counts + pyramid_offset(l),
                                                ix.state + pyramid_offset(l),
                                                l ? ix.state + pyramid_offset(l - 1) : nullptr, l, L,
                                                ix.th_quad, nc, ix.scalars);
   }
-  k_leaf_flags<<<blocks_for(ncap), TPB, 0, s>>>(ix.state, ix.scalars, ncap, flags, cell_lvl);
+  MKNN_LAUNCH k_leaf_flags<<<blocks_for(ncap), TPB, 0, s>>>(ix.state, ix.scalars, ncap, flags, cell_lvl);
   MKNN_CUDA_OK(cudaGetLastError());
   int rc = exclusive_scan_i32(flags, ordx, ncap, scratch, s);
   if (rc) return rc;
-  k_leaf_table<<<blocks_for(ncap), TPB, 0, s>>>(flags, ordx, cell_lvl, ix.counts, ix.scalars, ncap,
+  MKNN_LAUNCH k_leaf_table<<<blocks_for(ncap), TPB, 0, s>>>(flags, ordx, cell_lvl, ix.counts, ix.scalars, ncap,
                                                 ix.z_map, ix.leaf_level, ix.leaf_code, ix.leaf_key,
                                                 ix.leaf_span, ix.build_counts);
   MKNN_CUDA_OK(cudaGetLastError());
@@ -272,13 +272,13 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
   MKNN_CUDA_OK(cudaMemsetAsync(st.cell_count, 0, sizeof(int32_t) * (ncap + 1), s));
   MKNN_CUDA_OK(cudaMemsetAsync(st.cell_fill, 0, sizeof(int32_t) * (ncap + 1), s));
   if (n > 0)
-    k_obj_leaf<<<grid_stride_blocks(n), TPB, 0, s>>>(x, y, n, r, ix.scalars, ix.z_map, st.leaf,
+    MKNN_LAUNCH k_obj_leaf<<<grid_stride_blocks(n), TPB, 0, s>>>(x, y, n, r, ix.scalars, ix.z_map, st.leaf,
                                                      st.cell_count, dev_clamped);
   MKNN_CUDA_OK(cudaGetLastError());
   int rc = exclusive_scan_i32(st.cell_count, st.cell_start, ncap, scratch, s);
   if (rc) return rc;
   if (n > 0)
-    k_obj_scatter<<<grid_stride_blocks(n), TPB, 0, s>>>(ids, x, y, n, st.leaf, st.cell_start,
+    MKNN_LAUNCH k_obj_scatter<<<grid_stride_blocks(n), TPB, 0, s>>>(ids, x, y, n, st.leaf, st.cell_start,
                                                         st.cell_fill, st.xy, st.ids);
   MKNN_CUDA_OK(cudaGetLastError());
   return 0;
@@ -291,12 +291,12 @@ int queries_index(DevQueries& dq, const DevIndex& ix, const Region& r, const lon
   MKNN_CUDA_OK(cudaMemsetAsync(dq.qcount, 0, sizeof(int32_t) * (ncap + 1), s));
   MKNN_CUDA_OK(cudaMemsetAsync(dq.qfill, 0, sizeof(int32_t) * (ncap + 1), s));
   if (nq == 0) return 0;
-  k_obj_leaf<<<grid_stride_blocks(nq), TPB, 0, s>>>(qx, qy, nq, r, ix.scalars, ix.z_map, dq.leaf,
+  MKNN_LAUNCH k_obj_leaf<<<grid_stride_blocks(nq), TPB, 0, s>>>(qx, qy, nq, r, ix.scalars, ix.z_map, dq.leaf,
                                                     dq.qcount, nullptr);
   MKNN_CUDA_OK(cudaGetLastError());
   int rc = exclusive_scan_i32(dq.qcount, dq.qstart, ncap, scratch, s);
   if (rc) return rc;
-  k_q_scatter<<<grid_stride_blocks(nq), TPB, 0, s>>>(nq, dq.leaf, dq.qstart, dq.qfill, dq.order);
+  MKNN_LAUNCH k_q_scatter<<<grid_stride_blocks(nq), TPB, 0, s>>>(nq, dq.leaf, dq.qstart, dq.qfill, dq.order);
   MKNN_CUDA_OK(cudaGetLastError());
 
   // stable issuer order for emission (engine.py:713 / oracle.py:56)
@@ -307,12 +307,12 @@ int queries_index(DevQueries& dq, const DevIndex& ix, const Region& r, const lon
   MKNN_CUDA_OK(cudaStreamSynchronize(s));
   const uint64_t range = (uint64_t)mm[1] - (uint64_t)mm[0];
   const int bits = range ? 64 - __builtin_clzll(range) : 0;
-  k_issuer_keys<<<blocks_for(nq), TPB, 0, s>>>(qi, nq, dq.minmax, dq.keys, dq.vals);
+  MKNN_LAUNCH k_issuer_keys<<<blocks_for(nq), TPB, 0, s>>>(qi, nq, dq.minmax, dq.keys, dq.vals);
   MKNN_CUDA_OK(cudaGetLastError());
   bool alt = false;
   rc = radix_sort_pairs_u64(dq.keys, dq.vals, dq.keys_alt, dq.vals_alt, nq, bits, scratch, s, &alt);
   if (rc) return rc;
-  k_issuer_rows<<<blocks_for(nq), TPB, 0, s>>>(alt ? dq.keys_alt : dq.keys,
+  MKNN_LAUNCH k_issuer_rows<<<blocks_for(nq), TPB, 0, s>>>(alt ? dq.keys_alt : dq.keys,
                                                alt ? dq.vals_alt : dq.vals, nq, dq.minmax, dq.row,
                                                out_qids);
   MKNN_CUDA_OK(cudaGetLastError());

@@ -15,6 +15,12 @@ int fail_cuda(cudaError_t e, const char* expr, const char* file, int line);
 int fail_msg(int code, const std::string& msg);
 const char* last_error_text();
 
+// every kernel launch of the library is counted (bench.py reports the
+// number of our own launches inside its timed region)
+void note_launch();
+long long launch_count();
+#define MKNN_LAUNCH ::mknn::note_launch(),
+
 // error codes (C-ABI: 0 ok, < 0 error)
 constexpr int E_INVALID = -1;   // ValueError on the Python side
 constexpr int E_CUDA = -2;      // RuntimeError
@@ -134,7 +140,19 @@ struct SearchArgs {
   double* out_dist;       // [nq * k]
   QueryStats* stats;      // [nq] by leaf-grouped position
   int audit;
+  int force_warp;  // use the warp-per-query kernel even for k <= 32 (tests)
+  int debug_phase; // profiling only: 1 = own leaf only (results invalid)
+  // instrumentation: (dir, iteration, leaf) keys of every distance task
+  unsigned long long* task_keys;  // nullptr when off
+  unsigned long long* task_count;
+  int64_t task_cap;
 };
+
+// T from task keys: sorts keys in place (alt buffer) and sums the leaf
+// populations of distinct keys into *dev_T
+int streamed_records(unsigned long long* keys, unsigned long long* keys_alt, uint32_t* vals,
+                     uint32_t* vals_alt, int64_t n, const int32_t* cell_start,
+                     unsigned long long* dev_T, void* scratch, cudaStream_t s);
 
 int search_launch(const SearchArgs& a, cudaStream_t s);
 

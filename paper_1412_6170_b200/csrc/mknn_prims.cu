@@ -4,6 +4,7 @@
 // the counting sorts of objects and queries by leaf (quadindex.py:197-202,
 // engine.py:208) and the stable issuer-order emission (engine.py:713,
 // oracle.py:56).
+#include <atomic>
 #include <cstdio>
 #include <string>
 
@@ -27,6 +28,10 @@ int fail_msg(int code, const std::string& msg) {
 }
 
 const char* last_error_text() { return g_err.c_str(); }
+
+static std::atomic<long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 // ------------------------------------------------------------------ scan
 namespace {
@@ -124,15 +129,15 @@ __global__ void k_set_zero_total(TO* out) { out[0] = 0; }
 template <typename TO>
 int exclusive_scan_impl(const int32_t* in, TO* out, int64_t n, void* scratch, cudaStream_t s) {
   if (n == 0) {
-    k_set_zero_total<TO><<<1, 1, 0, s>>>(out);
+    MKNN_LAUNCH k_set_zero_total<TO><<<1, 1, 0, s>>>(out);
     MKNN_CUDA_OK(cudaGetLastError());
     return 0;
   }
   const int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
   long long* sums = (long long*)scratch;
-  k_tile_sums<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, n, sums);
-  k_scan_sums<<<1, 1024, 0, s>>>(sums, nb);
-  k_tile_apply<TO><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, out, n, sums);
+  MKNN_LAUNCH k_tile_sums<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, n, sums);
+  MKNN_LAUNCH k_scan_sums<<<1, 1024, 0, s>>>(sums, nb);
+  MKNN_LAUNCH k_tile_apply<TO><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, out, n, sums);
   MKNN_CUDA_OK(cudaGetLastError());
   return 0;
 }
@@ -260,10 +265,10 @@ int radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uin
   uint64_t *ki = keys, *ko = keys_alt;
   uint32_t *vi = vals, *vo = vals_alt;
   for (int shift = 0; shift < bits; shift += 8) {
-    k_radix_hist<<<(unsigned)nb, RX_THREADS, 0, s>>>(ki, n, shift, hist, nb);
+    MKNN_LAUNCH k_radix_hist<<<(unsigned)nb, RX_THREADS, 0, s>>>(ki, n, shift, hist, nb);
     int rc = exclusive_scan_i32(hist, offs, hn, sc, s);
     if (rc) return rc;
-    k_radix_scatter<<<(unsigned)nb, RX_THREADS, 0, s>>>(ki, vi, ko, vo, n, shift, offs, nb);
+    MKNN_LAUNCH k_radix_scatter<<<(unsigned)nb, RX_THREADS, 0, s>>>(ki, vi, ko, vo, n, shift, offs, nb);
     MKNN_CUDA_OK(cudaGetLastError());
     std::swap(ki, ko);
     std::swap(vi, vo);
@@ -300,11 +305,11 @@ __global__ void k_minmax(const int64_t* __restrict__ in, int64_t n, int64_t* out
 }  // namespace
 
 int minmax_i64(const int64_t* in, int64_t n, int64_t* dev_out, cudaStream_t s) {
-  k_minmax_init<<<1, 1, 0, s>>>(dev_out);
+  MKNN_LAUNCH k_minmax_init<<<1, 1, 0, s>>>(dev_out);
   if (n > 0) {
     int64_t blocks = (n + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
-    k_minmax<<<(unsigned)blocks, 256, 0, s>>>(in, n, dev_out);
+    MKNN_LAUNCH k_minmax<<<(unsigned)blocks, 256, 0, s>>>(in, n, dev_out);
   }
   MKNN_CUDA_OK(cudaGetLastError());
   return 0;

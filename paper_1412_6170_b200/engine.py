@@ -152,6 +152,9 @@ class Engine:
         self._h = None
         self._index_cache: QuadIndex | None = None
         self._index_tick = -1
+        # count the reference's streamed records T per tick (measurement only)
+        self._instrument = False
+        self.last_streamed_records = -1
 
     # -- lifecycle (engine.py:570-585) --------------------------------------
     def _handle(self):
@@ -170,7 +173,7 @@ class Engine:
                 x_lo=float(r.x_lo), y_lo=float(r.y_lo), x_hi=float(r.x_hi), y_hi=float(r.y_hi),
                 self_check=int(bool(self.config.self_check)),
                 audit_pruning=int(bool(self.config.audit_pruning)),
-                device=int(self.config.device), reserved=0)
+                device=int(self.config.device), instrument=int(self._instrument))
             h = ctypes.c_void_p()
             N.check(N.lib().mknn_create(ctypes.byref(cfg), ctypes.byref(h)), None, "mknn_create")
             self._h = h
@@ -192,6 +195,17 @@ class Engine:
             self.close()
         except Exception:
             pass
+
+    @property
+    def instrument(self) -> bool:
+        return self._instrument
+
+    @instrument.setter
+    def instrument(self, on: bool) -> None:
+        """Count T on the following ticks; measurement only."""
+        self._instrument = bool(on)
+        if self._h is not None:
+            N.check(N.lib().mknn_set_instrument(self._h, int(self._instrument)), self._h)
 
     def set_stream(self, stream) -> None:
         """Run on a torch.cuda.Stream (or raw cudaStream_t int)."""
@@ -258,6 +272,7 @@ class Engine:
             t_emit_us=m.t_emit_us)
         if m.rebuild_flag:
             self._last_build_tick = m.tick
+        self.last_streamed_records = m.streamed_records
         self.last_metrics = tm
         return tm
 

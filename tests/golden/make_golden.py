@@ -25,6 +25,7 @@ import numpy as np
 REF = "/root/reference/pkg/src"
 sys.path.insert(0, REF)
 
+import mknn.engine as _eng  # noqa: E402
 from mknn.engine import Engine, EngineConfig  # noqa: E402
 from mknn.geometry import Rect, encode_points, leaf_order_keys, morton_encode, Point  # noqa: E402,F401
 from mknn.oracle import brute_force_knn, compare_results  # noqa: E402
@@ -43,6 +44,27 @@ def digest(*arrays) -> str:
         h.update(str(a.shape).encode())
         h.update(a.tobytes())
     return h.hexdigest()
+
+
+# T: object records streamed by the distance tasks = the sum
+# of leaf populations over the runs that first_iteration / update_nn_lists
+# receive (engine.py:356-393).  Counted by wrapping both functions.
+_T = [0]
+_orig_first, _orig_update = _eng.first_iteration, _eng.update_nn_lists
+
+
+def _first(run_leaf, starts, ends, qstore, ostore, *a, **kw):
+    _T[0] += int((ostore.cell_end[run_leaf] - ostore.cell_start[run_leaf]).sum())
+    return _orig_first(run_leaf, starts, ends, qstore, ostore, *a, **kw)
+
+
+def _update(run_leaf, run_starts, run_ends, refs2, qstore, ostore, *a, **kw):
+    _T[0] += int((ostore.cell_end[run_leaf] - ostore.cell_start[run_leaf]).sum())
+    return _orig_update(run_leaf, run_starts, run_ends, refs2, qstore, ostore, *a, **kw)
+
+
+_eng.first_iteration = _first
+_eng.update_nn_lists = _update
 
 
 def metrics_dict(m) -> dict:
@@ -71,13 +93,15 @@ def run_case(name, region, k, ticks, th_quad="auto", l_max=10, kind="tick",
             qx = np.asarray(qx, np.float64); qy = np.asarray(qy, np.float64)
             for key, a in (("ids", ids), ("x", x), ("y", y), ("qi", qi), ("qx", qx), ("qy", qy)):
                 arrs[f"t{t}_{key}"] = a
+            _T[0] = 0
             res = eng.process_tick(ids, x, y, qi, qx, qy)
             m = eng.last_metrics
             orc = brute_force_knn(ids, x, y, qi, qx, qy, k)
             rep = compare_results(res, orc, positions=(ids, x, y))
             assert rep.ok, f"{name}: reference engine disagrees with its oracle"
             assert np.array_equal(res.distances, orc.distances)
-            tmeta = dict(metrics=metrics_dict(m), verdicts=rep.counts,
+            tmeta = dict(metrics=dict(metrics_dict(m), streamed_records=_T[0]),
+                         verdicts=rep.counts,
                          oracle_digest=digest(orc.query_ids, orc.lengths, orc.neighbour_ids,
                                               orc.distances),
                          engine_digest=digest(res.query_ids, res.lengths, res.neighbour_ids,
@@ -213,12 +237,13 @@ def main():
     cfg1 = dict(input_digest=digest(x, y))
     arrs = {}
     with Engine(EngineConfig(k=8, region=R22)) as eng:
+        _T[0] = 0
         res = eng.process_tick(ids, x, y, ids[sel], x[sel], y[sel])
         m = eng.last_metrics
     orc = brute_force_knn(ids, x, y, ids[sel], x[sel], y[sel], 8)
     rep = compare_results(res, orc, positions=(ids, x, y))
     assert rep.ok
-    cfg1.update(metrics=metrics_dict(m), verdicts=rep.counts,
+    cfg1.update(metrics=dict(metrics_dict(m), streamed_records=_T[0]), verdicts=rep.counts,
                 oracle_digest=digest(orc.query_ids, orc.lengths, orc.neighbour_ids, orc.distances),
                 index=dict(l_deep=eng.index.l_deep, n_leaves=eng.index.n_leaves,
                            overfull_leaves=eng.index.overfull_leaves))

@@ -44,6 +44,7 @@ def engine_for(case):
 def test_golden_case(name):
     case = G.load(name)
     with engine_for(case) as eng:
+        eng.instrument = True
         for t, tick in enumerate(case.ticks):
             res = eng.process_tick(tick.ids, tick.x, tick.y, tick.qi, tick.qx, tick.qy)
             assert G.result_digest(res) == tick.meta["oracle_digest"], f"tick {t}"
@@ -58,6 +59,7 @@ def test_golden_case(name):
                 for key in ("distance_evals", "pruned_leaves", "iterations_left",
                             "iterations_right", "active_left", "active_right"):
                     assert getattr(m, key) == want[key], (t, key, getattr(m, key), want[key])
+                assert eng.last_streamed_records == want["streamed_records"], t
             ix = eng.index
             wi = tick.meta["index"]
             assert ix.l_deep == wi["l_deep"] and ix.n_leaves == wi["n_leaves"]
@@ -77,6 +79,7 @@ def test_cfg1_matches_reference():
     snap = synth.place(100_000, "uniform", seed=0)
     sel = np.random.default_rng(1).choice(100_000, 10_000, replace=False)
     with Engine(EngineConfig(k=8, region=synth.REGION)) as eng:
+        eng.instrument = True
         res = eng.process_tick(snap.ids, snap.x, snap.y, snap.ids[sel], snap.x[sel], snap.y[sel])
         m = eng.last_metrics
         assert eng.index.n_leaves == meta["index"]["n_leaves"]
@@ -84,6 +87,7 @@ def test_cfg1_matches_reference():
     for key in ("distance_evals", "pruned_leaves", "iterations_left", "iterations_right",
                 "active_left", "active_right"):
         assert getattr(m, key) == meta["metrics"][key], key
+    assert eng.last_streamed_records == meta["metrics"]["streamed_records"]
 
 
 @pytest.mark.parametrize("k", [1, 2, 5, 8, 16, 31, 32, 33, 64, 100, 128, 129, 200, 256, 300, 512])

@@ -91,7 +91,7 @@ def test_engine_port_matches_reference(name):
         if name in DEGENERATE_TIES:
             continue
         for key in ("distance_evals", "pruned_leaves", "iterations_left", "iterations_right",
-                    "active_left", "active_right"):
+                    "active_left", "active_right", "streamed_records"):
             assert m[key] == want[key], (key, m[key], want[key])
 
 
