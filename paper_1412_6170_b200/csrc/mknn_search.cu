@@ -57,14 +57,12 @@ __device__ __forceinline__ void bitonic_step(double (&d)[KPL], long long (&id)[K
         const int t = s | js;
         const bool asc = ((s << 5) & size) == 0;
         const bool sw = asc ? key_less(d[t], id[t], d[s], id[s]) : key_less(d[s], id[s], d[t], id[t]);
-        if (sw) {
-          const double td = d[s];
-          d[s] = d[t];
-          d[t] = td;
-          const long long ti = id[s];
-          id[s] = id[t];
-          id[t] = ti;
-        }
+        const double ds = d[s], dt = d[t];
+        const long long is = id[s], it = id[t];
+        d[s] = sw ? dt : ds;
+        d[t] = sw ? ds : dt;
+        id[s] = sw ? it : is;
+        id[t] = sw ? is : it;
       }
     }
   } else {
@@ -77,10 +75,8 @@ __device__ __forceinline__ void bitonic_step(double (&d)[KPL], long long (&id)[K
       const bool lower = (lane & j) == 0;
       const bool take = (lower == asc) ? key_less(pd, pi, d[s], id[s])
                                        : key_less(d[s], id[s], pd, pi);
-      if (take) {
-        d[s] = pd;
-        id[s] = pi;
-      }
+      d[s] = take ? pd : d[s];
+      id[s] = take ? pi : id[s];
     }
   }
 }
@@ -104,10 +100,9 @@ __device__ __forceinline__ void bitonic_merge_into(List<KPL>& L, double (&cd)[KP
   for (int s = 0; s < KPL; s++) {
     const double rd = __shfl_xor_sync(FULL, cd[KPL - 1 - s], 31);
     const long long ri = __shfl_xor_sync(FULL, ci[KPL - 1 - s], 31);
-    if (key_less(rd, ri, L.d[s], L.id[s])) {
-      L.d[s] = rd;
-      L.id[s] = ri;
-    }
+    const bool lt2 = key_less(rd, ri, L.d[s], L.id[s]);
+    L.d[s] = lt2 ? rd : L.d[s];
+    L.id[s] = lt2 ? ri : L.id[s];
   }
 #pragma unroll
   for (int j = N >> 1; j > 0; j >>= 1) bitonic_step<KPL>(L.d, L.id, lane, N, j);
@@ -139,10 +134,10 @@ __device__ __forceinline__ void list_insert(List<KPL>& L, double kd, long long k
 #pragma unroll
   for (int s = 0; s < KPL; s++) {
     const bool gprev = lane ? ((m[s] >> (lane - 1)) & 1u) : (s > 0 ? (m[s > 0 ? s - 1 : 0] >> 31) & 1u : 0u);
-    if (gt[s]) {
-      L.d[s] = gprev ? pd[s] : kd;
-      L.id[s] = gprev ? pi[s] : ki;
-    }
+    const double nd = gprev ? pd[s] : kd;
+    const long long ni = gprev ? pi[s] : ki;
+    L.d[s] = gt[s] ? nd : L.d[s];
+    L.id[s] = gt[s] ? ni : L.id[s];
   }
 }
 
