@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -167,8 +168,9 @@ struct mknn_engine {
 
   DevIndex ix;
   bool have_index = false;
+  bool last_tick_ok = false;  // false: the store's sub-cell counters may be dirty
   int32_t h_l_deep = 0;
-  int64_t h_n_leaves = 0, h_overfull = 0, h_n_build = 0;
+  int64_t h_n_leaves = 0, h_overfull = 0, h_n_build = 0, h_n_sub = 0;
   DevStore st;
   DevQueries dq;
 
@@ -182,6 +184,7 @@ struct mknn_engine {
   int64_t* offsets = nullptr; int64_t cap_off = 0;
   long long* out_qids = nullptr; int64_t cap_oq = 0;
   QueryStats* stats = nullptr; int64_t cap_stats = 0;
+  unsigned long long* prof = nullptr;  // MKNN_PROF=1 work counters
   unsigned long long* counters = nullptr;  // [0] evals [1] prunes [2] viol [3] clamped
   uint32_t* hist = nullptr;                // 2 x hist_cap
   // instrumentation buffers (config.instrument & 1)
@@ -240,13 +243,10 @@ struct DevOut {
 
 int alloc_store(mknn_engine* h, int64_t n) {
   const int64_t ncap = int64_t(1) << (2 * h->cfg.l_max);
-  if (!h->st.cell_count) {
-    MKNN_CUDA_OK(cudaMalloc(&h->st.cell_count, sizeof(int32_t) * (ncap + 2)));
+  if (!h->st.cell_start) {
     MKNN_CUDA_OK(cudaMalloc(&h->st.cell_start, sizeof(int32_t) * (ncap + 2)));
-    MKNN_CUDA_OK(cudaMalloc(&h->st.cell_fill, sizeof(int32_t) * (ncap + 2)));
-    MKNN_CUDA_OK(cudaMalloc(&h->dq.qcount, sizeof(int32_t) * (ncap + 2)));
-    MKNN_CUDA_OK(cudaMalloc(&h->dq.qstart, sizeof(int32_t) * (ncap + 2)));
-    MKNN_CUDA_OK(cudaMalloc(&h->dq.qfill, sizeof(int32_t) * (ncap + 2)));
+    MKNN_CUDA_OK(cudaMalloc(&h->st.chunk_start, sizeof(int32_t) * (ncap + 2)));
+    MKNN_CUDA_OK(cudaMalloc(&h->st.nch, sizeof(int32_t) * (ncap + 2)));
     MKNN_CUDA_OK(cudaMalloc(&h->dq.minmax, sizeof(int64_t) * 2));
     MKNN_CUDA_OK(cudaMalloc(&h->counters, sizeof(unsigned long long) * 8));
     h->hist_cap = (int)(ncap + 2);
@@ -254,16 +254,16 @@ int alloc_store(mknn_engine* h, int64_t n) {
   }
   if (n > h->st.cap) {
     int64_t nc = std::max<int64_t>(n, h->st.cap * 3 / 2);
-    cudaFree(h->st.xy);
-    cudaFree(h->st.ids);
-    cudaFree(h->st.leaf);
-    h->st.xy = nullptr;
-    h->st.ids = nullptr;
-    h->st.leaf = nullptr;
+    cudaFree(h->st.obj);
+    cudaFree(h->st.rec);
+    cudaFree(h->st.key);
+    h->st.rec = nullptr;
+    h->st.obj = nullptr;
+    h->st.key = nullptr;
     h->st.cap = 0;
-    MKNN_CUDA_OK(cudaMalloc(&h->st.xy, sizeof(double2) * nc));
-    MKNN_CUDA_OK(cudaMalloc(&h->st.ids, sizeof(long long) * nc));
-    MKNN_CUDA_OK(cudaMalloc(&h->st.leaf, sizeof(uint32_t) * nc));
+    MKNN_CUDA_OK(cudaMalloc(&h->st.obj, sizeof(StoreRec) * nc));
+    MKNN_CUDA_OK(cudaMalloc(&h->st.rec, sizeof(StoreRec) * nc));
+    MKNN_CUDA_OK(cudaMalloc(&h->st.key, sizeof(uint32_t) * nc));
     h->st.cap = nc;
   }
   return 0;
@@ -273,6 +273,7 @@ int alloc_queries(mknn_engine* h, int64_t nq) {
   if (nq <= h->dq.cap) return 0;
   const int64_t nc = std::max<int64_t>(nq, h->dq.cap * 3 / 2);
   cudaFree(h->dq.leaf);
+  cudaFree(h->dq.qkey);
   cudaFree(h->dq.order);
   cudaFree(h->dq.row);
   cudaFree(h->dq.keys);
@@ -281,6 +282,7 @@ int alloc_queries(mknn_engine* h, int64_t nq) {
   cudaFree(h->dq.vals_alt);
   h->dq.cap = 0;
   MKNN_CUDA_OK(cudaMalloc(&h->dq.leaf, sizeof(uint32_t) * nc));
+  MKNN_CUDA_OK(cudaMalloc(&h->dq.qkey, sizeof(uint32_t) * nc));
   MKNN_CUDA_OK(cudaMalloc(&h->dq.order, sizeof(uint32_t) * nc));
   MKNN_CUDA_OK(cudaMalloc(&h->dq.row, sizeof(uint32_t) * nc));
   MKNN_CUDA_OK(cudaMalloc(&h->dq.keys, sizeof(uint64_t) * nc));
@@ -299,6 +301,7 @@ int refresh_index_info(mknn_engine* h) {
   h->h_n_leaves = sc[1];
   h->h_overfull = sc[2];
   h->h_n_build = sc[3];
+  h->h_n_sub = sc[4];
   return 0;
 }
 
@@ -321,7 +324,8 @@ int core_tick(mknn_engine* h, int64_t n, const long long* ids, const double* x, 
     h->cap_rows = c;
   }
   const int64_t ncap = int64_t(1) << (2 * h->cfg.l_max);
-  size_t sb = std::max({scan_scratch_bytes(ncap + 2), scan_scratch_bytes(std::max<int64_t>(nq, 1) + 1),
+  size_t sb = std::max({scan_scratch_bytes(ncap + 2), scan_scratch_bytes(n + ncap + 2),
+                        scan_scratch_bytes(std::max<int64_t>(nq, 1) + 1),
                         radix_scratch_bytes(std::max<int64_t>(nq, 1))});
   if ((rc = h->scratch.ensure(sb + 1024))) return h->set_err(rc);
 
@@ -337,13 +341,19 @@ int core_tick(mknn_engine* h, int64_t n, const long long* ids, const double* x, 
     if ((rc = index_build(h->ix, h->r, x, y, n, h->scratch.p, s))) return h->set_err(rc);
     h->have_index = true;
     m.rebuild_flag = 1;
+    if ((rc = refresh_index_info(h))) return h->set_err(rc);  // leaf count sizes the store tables
   }
+  if ((rc = store_reserve(h->st, h->h_n_sub, h->h_n_leaves, n))) return h->set_err(rc);
+  if (!h->last_tick_ok) h->st.dirty = true;
+  h->last_tick_ok = false;
   MKNN_CUDA_OK(cudaEventRecord(h->ev[1], s));
   MKNN_CUDA_OK(cudaMemsetAsync(h->counters, 0, sizeof(unsigned long long) * 8, s));
-  if ((rc = store_index_objects(h->st, h->ix, h->r, ids, x, y, n, h->counters + 3, h->scratch.p, s)))
+  if ((rc = store_index_objects(h->st, h->ix, h->r, ids, x, y, n, h->h_n_leaves, h->h_n_sub,
+                                h->counters + 3, h->scratch.p, s)))
     return h->set_err(rc);
   MKNN_CUDA_OK(cudaEventRecord(h->ev[2], s));
-  if ((rc = queries_index(h->dq, h->ix, h->r, qi, qx, qy, nq, o.qids, h->scratch.p, s)))
+  if ((rc = queries_index(h->dq, h->st, h->ix, h->r, qi, qx, qy, nq, h->h_n_sub, o.qids,
+                          h->scratch.p, s)))
     return h->set_err(rc);
   MKNN_CUDA_OK(cudaEventRecord(h->ev[3], s));
 
@@ -356,8 +366,9 @@ int core_tick(mknn_engine* h, int64_t n, const long long* ids, const double* x, 
   a.leaf_key = h->ix.leaf_key;
   a.leaf_span = h->ix.leaf_span;
   a.cell_start = h->st.cell_start;
-  a.xy = h->st.xy;
-  a.ids = h->st.ids;
+  a.chunk_start = h->st.chunk_start;
+  a.box = h->st.box;
+  a.obj = h->st.obj;
   a.q_order = h->dq.order;
   a.q_leaf = h->dq.leaf;
   a.q_row = h->dq.row;
@@ -366,15 +377,19 @@ int core_tick(mknn_engine* h, int64_t n, const long long* ids, const double* x, 
   a.qy = qy;
   a.nq = nq;
   a.out_len = o.len;
-  a.out_nids = h->out_nids;
-  a.out_dist = h->out_dist;
+  a.out_nids = o.nids;  // padded rows in the output itself (rows_compact)
+  a.out_dist = o.dist;
   a.stats = h->stats;
   a.audit = h->cfg.audit_pruning;
   {
-    static const char* tp = getenv("MKNN_TPQ");
     static const char* dp = getenv("MKNN_DEBUG_PHASE");
-    a.force_warp = !(tp && tp[0] == '1');
     a.debug_phase = dp ? atoi(dp) : 0;
+    static const char* pf = getenv("MKNN_PROF");
+    if (pf && pf[0] == '1') {
+      if (!h->prof) MKNN_CUDA_OK(cudaMalloc(&h->prof, 8 * 16));
+      MKNN_CUDA_OK(cudaMemsetAsync(h->prof, 0, 8 * 16, s));
+      a.prof = h->prof;
+    }
   }
   const bool instr = (h->cfg.instrument & 1) != 0;
   if (instr) {
@@ -416,7 +431,7 @@ int core_tick(mknn_engine* h, int64_t n, const long long* ids, const double* x, 
   MKNN_CUDA_OK(cudaMemsetAsync(h->hist, 0, sizeof(uint32_t) * 2 * h->hist_cap, s));
   if ((rc = stats_reduce(h->stats, nq, h->counters, h->hist, h->hist + h->hist_cap, h->hist_cap, s)))
     return h->set_err(rc);
-  if ((rc = rows_compact(o.len, h->out_nids, h->out_dist, nq, k, o.offsets, o.nids, o.dist,
+  if ((rc = rows_compact(o.len, o.nids, o.dist, nq, k, o.offsets, h->out_nids, h->out_dist,
                          h->scratch.p, s)))
     return h->set_err(rc);
   MKNN_CUDA_OK(cudaEventRecord(h->ev[5], s));
@@ -426,9 +441,6 @@ int core_tick(mknn_engine* h, int64_t n, const long long* ids, const double* x, 
   int64_t total = 0;
   MKNN_CUDA_OK(cudaMemcpyAsync(&total, o.offsets + nq, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   MKNN_CUDA_OK(cudaStreamSynchronize(s));
-  if (rebuild) {
-    if ((rc = refresh_index_info(h))) return h->set_err(rc);
-  }
 
   // engine.py:661-663 active lists from navigate-call histograms
   for (int d = 0; d < 2; d++) {
@@ -469,11 +481,21 @@ int core_tick(mknn_engine* h, int64_t n, const long long* ids, const double* x, 
   m.t_loop_us = us_between(h->ev[3], h->ev[4]);
   m.t_emit_us = us_between(h->ev[4], h->ev[5]);
 
+  h->last_tick_ok = true;
   h->history.push_back(m.distance_evals);
   h->tick += 1;
   m.t_total_us = std::chrono::duration_cast<std::chrono::microseconds>(
                      std::chrono::steady_clock::now() - t_start)
                      .count();
+  if (a.prof) {  // profiling only (MKNN_PROF=1)
+    unsigned long long pv[8];
+    MKNN_CUDA_OK(cudaMemcpy(pv, h->prof, sizeof(pv), cudaMemcpyDeviceToHost));
+    fprintf(stderr,
+            "[mknn prof] per query: own chunks %.2f/%.2f, exp leaves %.2f, exp chunks %.2f/%.2f, "
+            "admitted %.2f, inserts %.2f, sort-merges %.2f\n",
+            (double)pv[0] / nq, (double)pv[5] / nq, (double)pv[4] / nq, (double)pv[1] / nq,
+            (double)pv[6] / nq, (double)pv[7] / nq, (double)pv[2] / nq, (double)pv[3] / nq);
+  }
   if (met) *met = m;
   return 0;
 }
@@ -694,14 +716,15 @@ void mknn_destroy(mknn_engine* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   index_free(h->ix);
-  void* ptrs[] = {h->st.xy, h->st.ids, h->st.leaf, h->st.cell_count, h->st.cell_start, h->st.cell_fill,
-                  h->dq.leaf, h->dq.order, h->dq.qcount, h->dq.qstart, h->dq.qfill, h->dq.row,
+  void* ptrs[] = {h->st.obj, h->st.rec, h->st.cursor, h->st.bstart, h->st.key, h->st.cell_start, h->st.chunk_start, h->st.nch,
+                  h->st.box, h->st.crange, h->st.cnt, h->st.kstart, 
+                  h->dq.leaf, h->dq.qkey, h->dq.order, h->dq.row,
                   h->dq.keys, h->dq.keys_alt, h->dq.vals, h->dq.vals_alt, h->dq.minmax,
                   h->in_ids, h->in_x, h->in_y, h->in_qi, h->in_qx, h->in_qy, h->out_len,
                   h->out_nids, h->out_dist, h->c_nids, h->c_dist, h->offsets, h->out_qids,
                   h->stats, h->counters, h->hist, h->snap_ids, h->snap_x, h->snap_y, h->hkeys,
                   h->hvals, h->winner, h->slot_of, h->d_nsnap, h->up_ids, h->up_x, h->up_y,
-                  h->tk, h->tk_alt, h->tk_cnt, h->tv, h->tv_alt};
+                  h->tk, h->tk_alt, h->tk_cnt, h->tv, h->tv_alt, h->prof};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   h->scratch.release();

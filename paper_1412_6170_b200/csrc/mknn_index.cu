@@ -26,6 +26,11 @@ namespace mknn {
 namespace {
 
 constexpr int TPB = 256;
+// store scatter (index_objects): tile size of the bucket partition, bucket count
+constexpr int PT_THREADS = 512;
+constexpr int PT_ITEMS = 4;
+constexpr int PT_TILE = PT_THREADS * PT_ITEMS;
+constexpr int PT_BUCKETS = 1024;
 
 inline unsigned blocks_for(int64_t n, int per = TPB) {
   int64_t b = (n + per - 1) / per;
@@ -123,20 +128,89 @@ __global__ void k_leaf_table(const int32_t* __restrict__ flags, const int32_t* _
   }
 }
 
-__global__ void k_obj_leaf(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
-                           Region r, const int32_t* __restrict__ scalars,
-                           const int32_t* __restrict__ z_map, uint32_t* __restrict__ leaf,
-                           int32_t* __restrict__ cell_count, unsigned long long* clamped) {
+// geometry.py:105-129 cell_coord for a given t (shared by two levels)
+__device__ __forceinline__ uint32_t coord_at(double t, int level) {
+  const double n = pow2_pos(level);
+  double c = floor(__dmul_rn(t, n));  // x 2^L is exact
+  c = fmax(c, 0.0);
+  c = fmin(c, n - 1.0);
+  return (uint32_t)c;
+}
+
+// Per point: the leaf (encode at l_deep -> z_map, quadindex.py:196-199;
+// engine.py:206) and the sub-cell key sub_base[leaf] + sub, where sub is the
+// point's Morton code s levels below the leaf's level.  The l_deep code is
+// the prefix of the level-16 code (floor(t * 2^16) >> d == floor(t * 2^(16-d))
+// for the same t, geometry.py:108-112), so both come from one normalisation.
+__device__ __forceinline__ void point_key(double xi, double yi, const Region& r, int l_deep,
+                                          const int32_t* __restrict__ z_map,
+                                          const uint8_t* __restrict__ leaf_level,
+                                          const uint8_t* __restrict__ sub_bits,
+                                          const int32_t* __restrict__ sub_base, uint32_t& leaf,
+                                          uint32_t& key) {
+  const double tx = (r.w > 0.0) ? __ddiv_rn(__dsub_rn(xi, r.x_lo), r.w) : 0.0;
+  const double ty = (r.h > 0.0) ? __ddiv_rn(__dsub_rn(yi, r.y_lo), r.h) : 0.0;
+  const uint32_t code = spread_bits32(coord_at(tx, l_deep)) | (spread_bits32(coord_at(ty, l_deep)) << 1);
+  leaf = (uint32_t)__ldg(&z_map[code]);
+  const int sb = __ldg(&sub_bits[leaf]);
+  uint32_t sub = 0;
+  if (sb) {
+    const uint32_t f = spread_bits32(coord_at(tx, 16)) | (spread_bits32(coord_at(ty, 16)) << 1);
+    const int lvl = __ldg(&leaf_level[leaf]);
+    sub = (f >> (2 * (16 - lvl) - sb)) & ((1u << sb) - 1u);
+  }
+  key = (uint32_t)__ldg(&sub_base[leaf]) + sub;
+}
+
+__global__ void k_point_keys(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                             Region r, const int32_t* __restrict__ scalars,
+                             const int32_t* __restrict__ z_map,
+                             const uint8_t* __restrict__ leaf_level,
+                             const uint8_t* __restrict__ sub_bits,
+                             const int32_t* __restrict__ sub_base, uint32_t* __restrict__ leaf_out,
+                             uint32_t* __restrict__ key_out, int32_t* __restrict__ cnt,
+                             unsigned long long* clamped, int bshift,
+                             int32_t* __restrict__ bucket_cnt) {
+  // bucket_cnt != nullptr: count coarse buckets (key >> bshift) through a
+  // block histogram instead of counting every key in global memory
+  __shared__ int bh[PT_BUCKETS];
+  if (bucket_cnt) {
+    for (int i = threadIdx.x; i < PT_BUCKETS; i += blockDim.x) bh[i] = 0;
+    __syncthreads();
+  }
   const int l_deep = scalars[0];
   unsigned out = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double xi = x[i], yi = y[i];
-    // geometry.py:215-220 count_outside
-    out += (xi < r.x_lo) | (xi > r.x_hi) | (yi < r.y_lo) | (yi > r.y_hi);
-    const uint32_t l = (uint32_t)z_map[encode(xi, yi, r, l_deep)];
-    leaf[i] = l;
-    atomicAdd(&cell_count[l], 1);
+  constexpr int U = 4;  // independent objects per thread per step (memory-level parallelism)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+    double xi[U], yi[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t i = i0 + u * stride;
+      xi[u] = i < n ? x[i] : r.x_lo;
+      yi[u] = i < n ? y[i] : r.y_lo;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t i = i0 + u * stride;
+      if (i < n) {
+        // geometry.py:215-220 count_outside
+        out += (xi[u] < r.x_lo) | (xi[u] > r.x_hi) | (yi[u] < r.y_lo) | (yi[u] > r.y_hi);
+        uint32_t leaf, key;
+        point_key(xi[u], yi[u], r, l_deep, z_map, leaf_level, sub_bits, sub_base, leaf, key);
+        if (leaf_out) leaf_out[i] = leaf;
+        key_out[i] = key;
+        if (bucket_cnt)
+          atomicAdd(&bh[key >> bshift], 1);
+        else
+          atomicAdd(&cnt[key], 1);
+      }
+    }
+  }
+  if (bucket_cnt) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < PT_BUCKETS; i += blockDim.x)
+      if (bh[i]) atomicAdd(&bucket_cnt[i], bh[i]);
   }
   if (clamped) {
 #pragma unroll
@@ -145,28 +219,210 @@ __global__ void k_obj_leaf(const double* __restrict__ x, const double* __restric
   }
 }
 
-__global__ void k_obj_scatter(const long long* __restrict__ ids, const double* __restrict__ x,
-                              const double* __restrict__ y, int64_t n,
-                              const uint32_t* __restrict__ leaf,
-                              const int32_t* __restrict__ cell_start, int32_t* __restrict__ fill,
-                              double2* __restrict__ sxy, long long* __restrict__ sids) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t l = leaf[i];
-    const int32_t slot = cell_start[l] + atomicAdd(&fill[l], 1);
-    sxy[slot] = make_double2(x[i], y[i]);
-    sids[slot] = ids[i];
+// exclusive scan of the bucket counts -> bucket starts (and partition cursors)
+__global__ void k_bucket_scan(const int32_t* __restrict__ bucket_cnt, int32_t* __restrict__ bstart,
+                              int32_t* __restrict__ cursor) {
+  __shared__ int wt[32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;  // PT_BUCKETS threads
+  const int v = bucket_cnt[t];
+  int inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) wt[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const int sv = lane < PT_BUCKETS / 32 ? wt[lane] : 0;
+    int si = sv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(FULL, si, o);
+      if (lane >= o) si += u;
+    }
+    wt[lane] = si - sv;
+  }
+  __syncthreads();
+  const int ex = inc - v + wt[w];
+  bstart[t] = ex;
+  cursor[t] = ex;
+  if (t == PT_BUCKETS - 1) bstart[PT_BUCKETS] = ex + v;
+}
+
+// Pass 1 of the store scatter: each tile of objects reserves, per coarse key
+// bucket, one contiguous run of the staging array (one global atomic per
+// tile and bucket) and writes its whole-sector records there.  Runs of
+// consecutive tiles in a bucket are adjacent, so L2 assembles full lines.
+__global__ void __launch_bounds__(PT_THREADS) k_partition(
+    const long long* __restrict__ ids, const double* __restrict__ x, const double* __restrict__ y,
+    const uint32_t* __restrict__ key, int64_t n, int bshift, int32_t* __restrict__ cursor,
+    StoreRec* __restrict__ out) {
+  __shared__ int hist[PT_BUCKETS], gbase[PT_BUCKETS];
+  const int t = threadIdx.x;
+  const int64_t base = (int64_t)blockIdx.x * PT_TILE;
+  const int tile_n = (n - base) < PT_TILE ? (int)(n - base) : PT_TILE;
+  for (int i = t; i < PT_BUCKETS; i += PT_THREADS) hist[i] = 0;
+  StoreRec rc[PT_ITEMS];
+#pragma unroll
+  for (int j = 0; j < PT_ITEMS; j++) {
+    const int li = t + j * PT_THREADS;
+    if (li < tile_n) {
+      const int64_t i = base + li;
+      rc[j].key = key[i];
+      rc[j].x = x[i];
+      rc[j].y = y[i];
+      rc[j].id = ids[i];
+      rc[j].pad = 0;
+    }
+  }
+  __syncthreads();
+  int rank[PT_ITEMS];
+#pragma unroll
+  for (int j = 0; j < PT_ITEMS; j++)
+    if (t + j * PT_THREADS < tile_n) rank[j] = atomicAdd(&hist[rc[j].key >> bshift], 1);
+  __syncthreads();
+  for (int i = t; i < PT_BUCKETS; i += PT_THREADS)
+    if (hist[i]) gbase[i] = atomicAdd(&cursor[i], hist[i]);
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < PT_ITEMS; j++)
+    if (t + j * PT_THREADS < tile_n) out[gbase[rc[j].key >> bshift] + rank[j]] = rc[j];
+}
+
+// Pass 2: one CTA per bucket: counting sort of the bucket's records by key
+// in shared memory (count, scan, scatter), writing kstart for the bucket's
+// keys and the records into their final slots (an L2-local window).
+constexpr int BS_THREADS = 512;
+
+__global__ void __launch_bounds__(BS_THREADS) k_bucket_sort(
+    const StoreRec* __restrict__ rec, const int32_t* __restrict__ bstart, int bshift, int64_t n_sub,
+    int32_t* __restrict__ kstart, StoreRec* __restrict__ obj) {
+  extern __shared__ int sh[];  // 2^bshift counters
+  __shared__ int wt[BS_THREADS / 32 + 1];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int b = blockIdx.x;
+  const int bs = bstart[b], be = bstart[b + 1];
+  const int64_t k0 = (int64_t)b << bshift;
+  if (k0 >= n_sub) return;
+  const int kw = (int)min((int64_t)1 << bshift, n_sub - k0);
+  for (int i = t; i < kw; i += BS_THREADS) sh[i] = 0;
+  __syncthreads();
+  for (int i = bs + t; i < be; i += BS_THREADS) atomicAdd(&sh[rec[i].key - k0], 1);
+  __syncthreads();
+  // exclusive scan of sh[0..kw): thread t owns a contiguous run
+  const int per = (kw + BS_THREADS - 1) / BS_THREADS;
+  const int lo = min(t * per, kw), hi = min(lo + per, kw);
+  int sum = 0;
+  for (int i = lo; i < hi; i++) sum += sh[i];
+  int inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) wt[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const int sv = lane < BS_THREADS / 32 ? wt[lane] : 0;
+    int si = sv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(FULL, si, o);
+      if (lane >= o) si += u;
+    }
+    if (lane < BS_THREADS / 32) wt[lane] = si - sv;
+  }
+  __syncthreads();
+  int run = bs + inc - sum + wt[w];
+  for (int i = lo; i < hi; i++) {
+    const int c = sh[i];
+    sh[i] = run;
+    kstart[k0 + i] = run;
+    run += c;
+  }
+  if (k0 + kw == n_sub && hi == kw && lo < hi) kstart[n_sub] = run;
+  __syncthreads();
+  for (int i = bs + t; i < be; i += BS_THREADS) {
+    const StoreRec rc = rec[i];
+    obj[atomicAdd(&sh[rc.key - k0], 1)] = rc;
   }
 }
 
-__global__ void k_q_scatter(int64_t nq, const uint32_t* __restrict__ leaf,
-                            const int32_t* __restrict__ qstart, int32_t* __restrict__ fill,
+__global__ void k_q_scatter(int64_t nq, const uint32_t* __restrict__ key,
+                            const int32_t* __restrict__ start, int32_t* __restrict__ cnt,
                             uint32_t* __restrict__ order) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t l = leaf[i];
-    order[qstart[l] + atomicAdd(&fill[l], 1)] = (uint32_t)i;
+    const uint32_t kk = key[i];
+    order[start[kk] + atomicSub(&cnt[kk], 1) - 1] = (uint32_t)i;
   }
+}
+
+// leaf ranges from the sub-cell starts: cell_start[l] and chunks per leaf
+__global__ void k_leaf_ranges(const int32_t* __restrict__ kstart, const int32_t* __restrict__ sub_base,
+                              int64_t n_leaves, int32_t* __restrict__ cell_start,
+                              int32_t* __restrict__ nch) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l <= n_leaves) {
+    const int32_t b = kstart[sub_base[l]];
+    cell_start[l] = b;
+    if (l < n_leaves) nch[l] = (kstart[sub_base[l + 1]] - b + CHUNK - 1) / CHUNK;
+  }
+}
+
+// per leaf: the object range of each of its chunks
+__global__ void k_chunk_ranges(const int32_t* __restrict__ cell_start,
+                               const int32_t* __restrict__ chunk_start, int64_t n_leaves,
+                               int2* __restrict__ crange) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l < n_leaves) {
+    const int b = cell_start[l], e = cell_start[l + 1];
+    int c = chunk_start[l];
+    for (int o = b; o < e; o += CHUNK, c++) crange[c] = make_int2(o, min(o + CHUNK, e));
+  }
+}
+
+// one thread per chunk: point bounding box (a chunk is 1 KB of contiguous
+// records, so each thread's loads stream through its own L1 lines)
+__global__ void k_chunk_boxes(const StoreRec* __restrict__ obj, const int2* __restrict__ crange,
+                              const int32_t* __restrict__ n_chunks_dev, ChunkBox* __restrict__ box) {
+  const int64_t nc = *n_chunks_dev;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nc;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int2 rg = crange[c];
+    double xl = DINF, yl = DINF, xh = -DINF, yh = -DINF;
+    for (int o = rg.x; o < rg.y; o++) {
+      const double2 p = *reinterpret_cast<const double2*>(&obj[o]);
+      xl = fmin(xl, p.x);
+      xh = fmax(xh, p.x);
+      yl = fmin(yl, p.y);
+      yh = fmax(yh, p.y);
+    }
+    box[c] = ChunkBox{xl, yl, xh, yh};
+  }
+}
+
+// rebuild: 4^s sub-cells per leaf with s the smallest level count that
+// leaves <= 4 build-time objects per sub-cell (s <= 5)
+__global__ void k_leaf_subs(const int32_t* __restrict__ build_counts,
+                            const int32_t* __restrict__ scalars, int64_t ncap,
+                            uint8_t* __restrict__ sub_bits, int32_t* __restrict__ sub_size) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= ncap) return;
+  if (l >= scalars[1]) {
+    sub_size[l] = 0;
+    return;
+  }
+  const int c = build_counts[l];
+  int sl = 0;
+  while (sl < 5 && c > (4 << (2 * sl))) sl++;
+  sub_bits[l] = (uint8_t)(2 * sl);
+  sub_size[l] = 1 << (2 * sl);
+}
+
+__global__ void k_store_scalar(int32_t* scalars, const int32_t* __restrict__ src, int64_t idx) {
+  scalars[4] = src[idx];
 }
 
 __global__ void k_issuer_keys(const long long* __restrict__ qi, int64_t nq,
@@ -212,6 +468,8 @@ int index_alloc(DevIndex& ix, int l_max, int th_quad) {
   MKNN_CUDA_OK(cudaMalloc(&ix.leaf_span, sizeof(uint32_t) * ncap));
   MKNN_CUDA_OK(cudaMalloc(&ix.build_counts, sizeof(int32_t) * ncap));
   MKNN_CUDA_OK(cudaMalloc(&ix.scalars, sizeof(int32_t) * 8));
+  MKNN_CUDA_OK(cudaMalloc(&ix.leaf_sub_bits, ncap));
+  MKNN_CUDA_OK(cudaMalloc(&ix.leaf_sub_base, sizeof(int32_t) * (ncap + 1)));
   return 0;
 }
 
@@ -226,6 +484,8 @@ void index_free(DevIndex& ix) {
   cudaFree(ix.leaf_span);
   cudaFree(ix.build_counts);
   cudaFree(ix.scalars);
+  cudaFree(ix.leaf_sub_bits);
+  cudaFree(ix.leaf_sub_base);
   ix = DevIndex{};
 }
 
@@ -259,44 +519,115 @@ int index_build(DevIndex& ix, const Region& r, const double* x, const double* y,
                                                 ix.z_map, ix.leaf_level, ix.leaf_code, ix.leaf_key,
                                                 ix.leaf_span, ix.build_counts);
   MKNN_CUDA_OK(cudaGetLastError());
+  // store ordering tables (sub-cells per leaf, their key ranges)
+  MKNN_LAUNCH k_leaf_subs<<<blocks_for(ncap), TPB, 0, s>>>(ix.build_counts, ix.scalars, ncap,
+                                                          ix.leaf_sub_bits, flags);
+  MKNN_CUDA_OK(cudaGetLastError());
+  rc = exclusive_scan_i32(flags, ix.leaf_sub_base, ncap, scratch, s);
+  if (rc) return rc;
+  MKNN_LAUNCH k_store_scalar<<<1, 1, 0, s>>>(ix.scalars, ix.leaf_sub_base, ncap);
+  MKNN_CUDA_OK(cudaGetLastError());
   // n_build for should_rebuild bookkeeping
   int32_t nb = (int32_t)std::min<int64_t>(n, 0x7fffffff);
   MKNN_CUDA_OK(cudaMemcpyAsync(ix.scalars + 3, &nb, sizeof(int32_t), cudaMemcpyHostToDevice, s));
   return 0;
 }
 
+int store_reserve(DevStore& st, int64_t n_sub, int64_t n_leaves, int64_t n) {
+  const int64_t need = std::max<int64_t>(n_sub, 1) + 2;
+  if (need > st.cap_sub) {
+    cudaFree(st.cnt);
+    cudaFree(st.kstart);
+    st.cnt = st.kstart = nullptr;
+    st.cap_sub = 0;
+    const int64_t c = std::max<int64_t>(need, st.cap_sub * 3 / 2);
+    MKNN_CUDA_OK(cudaMalloc(&st.cnt, sizeof(int32_t) * c));
+    MKNN_CUDA_OK(cudaMalloc(&st.kstart, sizeof(int32_t) * c));
+    st.cap_sub = c;
+    st.dirty = true;
+  }
+  const int64_t nbox = n / CHUNK + n_leaves + 1;
+  if (!st.cursor) {
+    MKNN_CUDA_OK(cudaMalloc(&st.cursor, sizeof(int32_t) * (PT_BUCKETS + 1)));
+    MKNN_CUDA_OK(cudaMalloc(&st.bstart, sizeof(int32_t) * (PT_BUCKETS + 1)));
+  }
+  if (nbox > st.cap_box) {
+    cudaFree(st.box);
+    cudaFree(st.crange);
+    st.box = nullptr;
+    st.crange = nullptr;
+    st.cap_box = 0;
+    const int64_t c = std::max<int64_t>(nbox, st.cap_box * 3 / 2);
+    MKNN_CUDA_OK(cudaMalloc(&st.box, sizeof(ChunkBox) * c));
+    MKNN_CUDA_OK(cudaMalloc(&st.crange, sizeof(int2) * c));
+    st.cap_box = c;
+  }
+  return 0;
+}
+
 int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const long long* ids,
-                        const double* x, const double* y, int64_t n,
-                        unsigned long long* dev_clamped, void* scratch, cudaStream_t s) {
-  const int64_t ncap = int64_t(1) << (2 * ix.l_max);
-  MKNN_CUDA_OK(cudaMemsetAsync(st.cell_count, 0, sizeof(int32_t) * (ncap + 1), s));
-  MKNN_CUDA_OK(cudaMemsetAsync(st.cell_fill, 0, sizeof(int32_t) * (ncap + 1), s));
+                        const double* x, const double* y, int64_t n, int64_t n_leaves,
+                        int64_t n_sub, unsigned long long* dev_clamped, void* scratch,
+                        cudaStream_t s) {
+  if (st.dirty) {
+    MKNN_CUDA_OK(cudaMemsetAsync(st.cnt, 0, sizeof(int32_t) * st.cap_sub, s));
+    st.dirty = false;
+  }
+  int bshift = 0;
+  while ((std::max<int64_t>(n_sub, 1) - 1) >> bshift >= PT_BUCKETS) bshift++;
+  const int nb = (int)(((std::max<int64_t>(n_sub, 1) - 1) >> bshift) + 1);
+  MKNN_CUDA_OK(cudaMemsetAsync(st.cursor, 0, sizeof(int32_t) * PT_BUCKETS, s));
   if (n > 0)
-    MKNN_LAUNCH k_obj_leaf<<<grid_stride_blocks(n), TPB, 0, s>>>(x, y, n, r, ix.scalars, ix.z_map, st.leaf,
-                                                     st.cell_count, dev_clamped);
+    MKNN_LAUNCH k_point_keys<<<grid_stride_blocks(n), TPB, 0, s>>>(
+        x, y, n, r, ix.scalars, ix.z_map, ix.leaf_level, ix.leaf_sub_bits, ix.leaf_sub_base,
+        nullptr, st.key, nullptr, dev_clamped, bshift, st.cursor);
   MKNN_CUDA_OK(cudaGetLastError());
-  int rc = exclusive_scan_i32(st.cell_count, st.cell_start, ncap, scratch, s);
+  MKNN_LAUNCH k_bucket_scan<<<1, PT_BUCKETS, 0, s>>>(st.cursor, st.bstart, st.cursor);
+  if (n > 0) {
+    MKNN_LAUNCH k_partition<<<(unsigned)((n + PT_TILE - 1) / PT_TILE), PT_THREADS, 0, s>>>(
+        ids, x, y, st.key, n, bshift, st.cursor, st.rec);
+    MKNN_CUDA_OK(cudaGetLastError());
+  }
+  const size_t bs_smem = sizeof(int32_t) << bshift;
+  if (bs_smem > 48 * 1024) {
+    static size_t configured = 0;
+    if (bs_smem > configured) {
+      MKNN_CUDA_OK(cudaFuncSetAttribute(k_bucket_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)bs_smem));
+      configured = bs_smem;
+    }
+  }
+  MKNN_LAUNCH k_bucket_sort<<<nb, BS_THREADS, bs_smem, s>>>(st.rec, st.bstart, bshift, n_sub,
+                                                           st.kstart, st.obj);
+  MKNN_CUDA_OK(cudaGetLastError());
+  MKNN_LAUNCH k_leaf_ranges<<<blocks_for(n_leaves + 1), TPB, 0, s>>>(st.kstart, ix.leaf_sub_base,
+                                                                    n_leaves, st.cell_start, st.nch);
+  MKNN_CUDA_OK(cudaGetLastError());
+  int rc = exclusive_scan_i32(st.nch, st.chunk_start, n_leaves, scratch, s);
   if (rc) return rc;
-  if (n > 0)
-    MKNN_LAUNCH k_obj_scatter<<<grid_stride_blocks(n), TPB, 0, s>>>(ids, x, y, n, st.leaf, st.cell_start,
-                                                        st.cell_fill, st.xy, st.ids);
+  if (n > 0) {
+    MKNN_LAUNCH k_chunk_ranges<<<blocks_for(n_leaves), TPB, 0, s>>>(st.cell_start, st.chunk_start,
+                                                                   n_leaves, st.crange);
+    const int64_t maxc = n / CHUNK + n_leaves + 1;
+    MKNN_LAUNCH k_chunk_boxes<<<blocks_for(maxc), TPB, 0, s>>>(st.obj, st.crange,
+                                                              st.chunk_start + n_leaves, st.box);
+  }
   MKNN_CUDA_OK(cudaGetLastError());
   return 0;
 }
 
-int queries_index(DevQueries& dq, const DevIndex& ix, const Region& r, const long long* qi,
-                  const double* qx, const double* qy, int64_t nq, long long* out_qids,
-                  void* scratch, cudaStream_t s) {
-  const int64_t ncap = int64_t(1) << (2 * ix.l_max);
-  MKNN_CUDA_OK(cudaMemsetAsync(dq.qcount, 0, sizeof(int32_t) * (ncap + 1), s));
-  MKNN_CUDA_OK(cudaMemsetAsync(dq.qfill, 0, sizeof(int32_t) * (ncap + 1), s));
+int queries_index(DevQueries& dq, DevStore& st, const DevIndex& ix, const Region& r,
+                  const long long* qi, const double* qx, const double* qy, int64_t nq,
+                  int64_t n_sub, long long* out_qids, void* scratch, cudaStream_t s) {
   if (nq == 0) return 0;
-  MKNN_LAUNCH k_obj_leaf<<<grid_stride_blocks(nq), TPB, 0, s>>>(qx, qy, nq, r, ix.scalars, ix.z_map, dq.leaf,
-                                                    dq.qcount, nullptr);
+  MKNN_LAUNCH k_point_keys<<<grid_stride_blocks(nq), TPB, 0, s>>>(
+      qx, qy, nq, r, ix.scalars, ix.z_map, ix.leaf_level, ix.leaf_sub_bits, ix.leaf_sub_base,
+      dq.leaf, dq.qkey, st.cnt, nullptr, 0, nullptr);
   MKNN_CUDA_OK(cudaGetLastError());
-  int rc = exclusive_scan_i32(dq.qcount, dq.qstart, ncap, scratch, s);
+  int rc = exclusive_scan_i32(st.cnt, st.kstart, n_sub, scratch, s);
   if (rc) return rc;
-  MKNN_LAUNCH k_q_scatter<<<grid_stride_blocks(nq), TPB, 0, s>>>(nq, dq.leaf, dq.qstart, dq.qfill, dq.order);
+  MKNN_LAUNCH k_q_scatter<<<grid_stride_blocks(nq), TPB, 0, s>>>(nq, dq.qkey, st.kstart, st.cnt,
+                                                                dq.order);
   MKNN_CUDA_OK(cudaGetLastError());
 
   // stable issuer order for emission (engine.py:713 / oracle.py:56)

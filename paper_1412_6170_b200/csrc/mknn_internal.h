@@ -57,7 +57,11 @@ struct DevIndex {
   uint32_t* leaf_key = nullptr;
   uint32_t* leaf_span = nullptr;
   int32_t* build_counts = nullptr;
-  int32_t* scalars = nullptr;  // [0] l_deep, [1] n_leaves, [2] overfull, [3] n_build
+  int32_t* scalars = nullptr;  // [0] l_deep, [1] n_leaves, [2] overfull, [3] n_build, [4] n_sub
+  // store ordering inside each leaf: 4^s sub-cells per leaf (s from the
+  // leaf's build count), leaf l owns sub-cell keys [sub_base[l], sub_base[l+1])
+  uint8_t* leaf_sub_bits = nullptr;  // 2*s
+  int32_t* leaf_sub_base = nullptr;  // 4^l_max + 1
   int l_max = 0;
   int th_quad = 0;
 };
@@ -71,30 +75,59 @@ void index_free(DevIndex& ix);
 int index_build(DevIndex& ix, const Region& r, const double* x, const double* y, int64_t n,
                 void* scratch, cudaStream_t s);
 
-// Per-tick object store (quadindex.py:166-213), leaf-sorted.
-struct DevStore {
-  double2* xy = nullptr;     // leaf-sorted positions
-  long long* ids = nullptr;  // leaf-sorted ids
-  uint32_t* leaf = nullptr;  // leaf ordinal per input object
-  int32_t* cell_count = nullptr;  // 4^l_max + 1
-  int32_t* cell_start = nullptr;  // 4^l_max + 2 (start[L] = n)
-  int32_t* cell_fill = nullptr;
-  int64_t cap = 0;
+// Per-tick object store (quadindex.py:166-213), leaf-grouped.  Inside a
+// leaf, objects are ordered by Morton sub-cell below the leaf's own level and
+// cut into chunks of CHUNK consecutive objects whose point bounding boxes let
+// the search skip chunks that cannot hold a neighbour (exact: see
+// mknn_search.cu).  Objects are 32-byte records (one L2 sector), so the
+// counting-sort scatter writes whole sectors and a candidate's position and
+// id arrive in one sector.
+constexpr int CHUNK = 32;
+
+struct ChunkBox {
+  double x_lo, y_lo, x_hi, y_hi;
 };
 
+struct __align__(32) StoreRec {  // one object of the leaf-sorted store
+  double x, y;
+  long long id;
+  uint32_t key, pad;
+};
+
+struct DevStore {
+  StoreRec* obj = nullptr;        // leaf-sorted objects
+  StoreRec* rec = nullptr;        // staging of the bucket partition pass
+  uint32_t* key = nullptr;        // sub-cell key per input object / query
+  int64_t cap = 0;
+  int32_t* cell_start = nullptr;  // 4^l_max + 2 (start[L] = n)
+  int32_t* chunk_start = nullptr; // 4^l_max + 2 (chunk ordinal of each leaf's first chunk)
+  int32_t* nch = nullptr;         // 4^l_max + 2 scratch (chunks per leaf)
+  ChunkBox* box = nullptr;        // per chunk
+  int2* crange = nullptr;         // per chunk: object range
+  int64_t cap_box = 0;
+  int32_t* cnt = nullptr;         // n_sub + 2; all zero between ticks
+  int32_t* kstart = nullptr;      // n_sub + 2
+  int32_t* cursor = nullptr;      // bucket counts / cursors of the partition pass
+  int32_t* bstart = nullptr;      // bucket starts
+  int64_t cap_sub = 0;
+  bool dirty = true;              // cnt must be cleared before use
+};
+
+// (re)size the sub-cell tables and chunk arrays for n objects
+int store_reserve(DevStore& st, int64_t n_sub, int64_t n_leaves, int64_t n);
+
 // quadindex.py:190-213 index_objects; clamped count accumulates into
-// dev_counters[0] (int64, device)
+// dev_clamped (u64, device).  n_leaves / n_sub are host copies.
 int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const long long* ids,
-                        const double* x, const double* y, int64_t n, unsigned long long* dev_clamped,
-                        void* scratch, cudaStream_t s);
+                        const double* x, const double* y, int64_t n, int64_t n_leaves,
+                        int64_t n_sub, unsigned long long* dev_clamped, void* scratch,
+                        cudaStream_t s);
 
 // engine.py:201-217 index_queries (leaf ordinal + leaf-grouped order)
 struct DevQueries {
   uint32_t* leaf = nullptr;     // own leaf per query (input order)
-  uint32_t* order = nullptr;    // queries grouped by leaf
-  int32_t* qcount = nullptr;    // per leaf
-  int32_t* qstart = nullptr;
-  int32_t* qfill = nullptr;
+  uint32_t* qkey = nullptr;     // (leaf << sub_bits) | sub per query
+  uint32_t* order = nullptr;    // queries grouped by leaf, sub-cell order inside
   uint32_t* row = nullptr;      // emission row per query (stable issuer rank)
   uint64_t* keys = nullptr;     // radix buffers
   uint64_t* keys_alt = nullptr;
@@ -104,9 +137,10 @@ struct DevQueries {
   int64_t cap = 0;
 };
 
-int queries_index(DevQueries& dq, const DevIndex& ix, const Region& r, const long long* qi,
-                  const double* qx, const double* qy, int64_t nq, long long* out_qids,
-                  void* scratch, cudaStream_t s);
+// uses st.sub_cnt / st.sub_start as its counting-sort tables
+int queries_index(DevQueries& dq, DevStore& st, const DevIndex& ix, const Region& r,
+                  const long long* qi, const double* qx, const double* qy, int64_t nq,
+                  int64_t n_sub, long long* out_qids, void* scratch, cudaStream_t s);
 
 // ------------------------------------------------------------- search
 struct QueryStats {
@@ -126,8 +160,9 @@ struct SearchArgs {
   const uint32_t* leaf_key;
   const uint32_t* leaf_span;
   const int32_t* cell_start;  // L + 1 entries
-  const double2* xy;
-  const long long* ids;
+  const int32_t* chunk_start; // L + 1 entries
+  const ChunkBox* box;
+  const StoreRec* obj;
   const uint32_t* q_order;
   const uint32_t* q_leaf;
   const uint32_t* q_row;
@@ -140,8 +175,9 @@ struct SearchArgs {
   double* out_dist;       // [nq * k]
   QueryStats* stats;      // [nq] by leaf-grouped position
   int audit;
-  int force_warp;  // use the warp-per-query kernel even for k <= 32 (tests)
   int debug_phase; // profiling only: 1 = own leaf only (results invalid)
+  // profiling only (MKNN_PROF=1): work counters, see PROF_* in mknn_search.cu
+  unsigned long long* prof;
   // instrumentation: (dir, iteration, leaf) keys of every distance task
   unsigned long long* task_keys;  // nullptr when off
   unsigned long long* task_count;
@@ -161,9 +197,11 @@ int search_launch(const SearchArgs& a, cudaStream_t s);
 int stats_reduce(const QueryStats* st, int64_t nq, unsigned long long* dev_tot, uint32_t* hist_l,
                  uint32_t* hist_r, int hist_cap, cudaStream_t s);
 
-// compact padded rows to CSR: offsets[nq + 1] (int64)
-int rows_compact(const int32_t* len, const long long* nids, const double* dist, int64_t nq, int k,
-                 int64_t* offsets, long long* c_nids, double* c_dist, void* scratch,
+// padded rows (written by the search into the output itself) -> CSR in
+// place: offsets[nq + 1] (int64); t_nids / t_dist are [nq * k] scratch
+// touched only when some row is short
+int rows_compact(const int32_t* len, long long* nids, double* dist, int64_t nq, int k,
+                 int64_t* offsets, long long* t_nids, double* t_dist, void* scratch,
                  cudaStream_t s);
 
 }  // namespace mknn

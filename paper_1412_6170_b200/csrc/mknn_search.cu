@@ -19,16 +19,26 @@
 // per-query navigate-call counts (stats_reduce).  Queries are processed in
 // leaf-grouped order so the warps of a CTA stream the same leaves through L1.
 //
+// Chunk pruning.  The store keeps each leaf's objects in sub-cell Morton
+// order cut into 32-object chunks with point bounding boxes (mknn_index.cu).
+// Every (query, leaf) row of the reference still counts the whole leaf in
+// distance_evals, but the warp only computes distances for chunks whose box
+// min-dist2 is <= the current k-th d2: a skipped chunk holds no object that
+// could be admitted, so the list -- and every later navigation decision that
+// reads its k-th d2 -- is exactly the reference's.  Chunks are visited
+// nearest box first, which fills the list with close objects early.
+//
 // Top-k.  The running list holds N = 32*KPL keys (N >= k) distributed as
 // element e = slot*32 + lane, sorted ascending by (d2, id) -- the oracle's
-// canonical order (oracle.py:76-77).  Each 32*KPL-candidate chunk of a leaf
-// is filtered against the k-th key (ballot); few survivors are inserted one
-// by one with warp shuffles, many are bitonic-sorted and bitonic-merged.
+// canonical order (oracle.py:76-77).  Each chunk is filtered against the
+// k-th key (ballot); few survivors are inserted one by one with warp
+// shuffles, many are bitonic-sorted and bitonic-merged.
 // Admission is (d2, id) < k-th and a quadrant is pruned only when its
 // min-dist2 is strictly greater than the k-th d2, so the canonical
 // lowest-id member of a boundary tie group is always found (the reference
 // prunes on >=, engine.py:447; distances are identical either way).
 #include <algorithm>
+#include <cstdlib>
 
 #include "mknn_internal.h"
 
@@ -36,7 +46,12 @@ namespace mknn {
 
 namespace {
 
-constexpr int WARPS_PER_CTA = 8;
+__device__ __forceinline__ double2 obj_xy(const StoreRec* __restrict__ obj, int i) {
+  return __ldg(reinterpret_cast<const double2*>(&obj[i]));
+}
+__device__ __forceinline__ long long obj_id(const StoreRec* __restrict__ obj, int i) {
+  return __ldg(&obj[i].id);
+}
 
 template <int KPL>
 struct List {
@@ -141,6 +156,82 @@ __device__ __forceinline__ void list_insert(List<KPL>& L, double kd, long long k
   }
 }
 
+// ---- one-slot lists (k <= 32): sorting networks on 32-bit keys ----------
+// akey(d2) = the float bits of d2 rounded down (monotone for d2 >= 0) with
+// the low `bits` bits replaced by a source index.  The networks below move
+// only these keys (one shuffle and one IMNMX per step instead of shuffling
+// and comparing fp64 + int64 pairs), then gather the exact (d2, id) by
+// source index.  trunc(akey(a)) < trunc(akey(b)) implies d2(a) < d2(b), so
+// the result is exactly in canonical (d2, id) order unless two neighbours
+// share a truncated key (a relative gap below 2^-17, or an exact tie such as
+// coincident objects); that case is detected and redone with the exact
+// (d2, id) network.
+constexpr uint32_t AKEY_INF = 0x7F800000u;
+
+__device__ __forceinline__ uint32_t akey(double d2, int bits, uint32_t src) {
+  return (__float_as_uint(__double2float_rd(d2)) & ~((1u << bits) - 1u)) | src;
+}
+
+// any two neighbours (lane, lane + 1) with equal truncated keys, other than
+// the +inf sentinels (which are all identical (inf, IDMAX) entries)?
+__device__ __forceinline__ bool akey_ties(uint32_t key, int bits, int lane) {
+  const uint32_t nk = __shfl_down_sync(FULL, key, 1);
+  const bool tie = lane < 31 && ((key ^ nk) >> bits) == 0 && (key >> bits) != (AKEY_INF >> bits);
+  return __any_sync(FULL, tie);
+}
+
+// sort one batch of 32 candidates (one per lane) ascending by (d2, id)
+__device__ __forceinline__ void batch_sort(double& d, long long& id, int lane) {
+  uint32_t key = akey(d, 5, (uint32_t)lane);
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int j = size >> 1; j > 0; j >>= 1) {
+      const uint32_t p = __shfl_xor_sync(FULL, key, j);
+      const bool take_min = ((lane & j) == 0) == ((lane & size) == 0);
+      key = take_min ? min(key, p) : max(key, p);
+    }
+  }
+  if (akey_ties(key, 5, lane)) {
+    double a[1] = {d};
+    long long b[1] = {id};
+    bitonic_sort<1>(a, b, lane);
+    d = a[0];
+    id = b[0];
+    return;
+  }
+  const int src = (int)(key & 31u);
+  const double nd = __shfl_sync(FULL, d, src);
+  const long long ni = __shfl_sync(FULL, id, src);
+  d = nd;
+  id = ni;
+}
+
+// L <- the 32 smallest of L u C, both ascending (one slot per lane)
+__device__ __forceinline__ void merge_list(List<1>& L, double cd, long long ci, int lane) {
+  const uint32_t kl = akey(L.d[0], 6, (uint32_t)lane);
+  const uint32_t kc = akey(cd, 6, 32u | (uint32_t)lane);
+  // min(A_i, B_{31-i}) holds the 32 smallest as a bitonic sequence
+  uint32_t m = min(kl, __shfl_sync(FULL, kc, 31 - lane));
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1) {
+    const uint32_t p = __shfl_xor_sync(FULL, m, j);
+    m = (lane & j) ? max(m, p) : min(m, p);
+  }
+  if (akey_ties(m, 6, lane)) {
+    double c[1] = {cd};
+    long long i[1] = {ci};
+    bitonic_merge_into<1>(L, c, i, lane);
+    return;
+  }
+  const int src = (int)(m & 31u);
+  const double dl = __shfl_sync(FULL, L.d[0], src), dc = __shfl_sync(FULL, cd, src);
+  const long long il = __shfl_sync(FULL, L.id[0], src), ic = __shfl_sync(FULL, ci, src);
+  const bool from_c = (m & 32u) != 0;
+  L.d[0] = from_c ? dc : dl;
+  L.id[0] = from_c ? ic : il;
+}
+
 // key of element k-1 (the current k-th neighbour; sentinel while not full)
 template <int KPL>
 __device__ __forceinline__ void list_kth(const List<KPL>& L, int k, double& kd, long long& ki) {
@@ -156,226 +247,139 @@ __device__ __forceinline__ void list_kth(const List<KPL>& L, int k, double& kd, 
   }
 }
 
-// engine.py:279-324 _merge_pack for one row: every object of [beg, end)
-// except the issuer (by id, engine.py:298-300) competes for the list.
-template <int KPL>
-__device__ __forceinline__ void scan_range(List<KPL>& L, int k, int beg, int end, double qx,
-                                           double qy, long long me, const double2* __restrict__ xy,
-                                           const long long* __restrict__ ids, int lane) {
-  constexpr int CH = 32 * KPL;
-  constexpr int INS_MAX = 12 + 4 * KPL;
-  for (int base = beg; base < end; base += CH) {
-    double kd;
-    long long ki;
-    list_kth<KPL>(L, k, kd, ki);
-    double cd[KPL];
-    long long ci[KPL];
-    unsigned mask[KPL];
-    int cnt = 0;
-#pragma unroll
-    for (int j = 0; j < KPL; j++) {
-      const int idx = base + j * 32 + lane;
-      bool pass = false;
-      double d2 = DINF;
-      long long id = IDMAX;
-      if (idx < end) {
-        const double2 p = __ldg(&xy[idx]);
-        d2 = pair_d2(qx, qy, p.x, p.y);
-        if (d2 <= kd && d2 < DINF) {
-          id = __ldg(&ids[idx]);
-          pass = (id != me) && key_less(d2, id, kd, ki);
-        }
-      }
-      cd[j] = pass ? d2 : DINF;
-      ci[j] = pass ? id : IDMAX;
-      mask[j] = __ballot_sync(FULL, pass);
-      cnt += __popc(mask[j]);
-    }
-    if (cnt == 0) continue;
-    if (cnt <= INS_MAX) {
-#pragma unroll
-      for (int j = 0; j < KPL; j++) {
-        unsigned m = mask[j];
-        while (m) {
-          const int src = __ffs(m) - 1;
-          m &= m - 1;
-          const double sd = __shfl_sync(FULL, cd[j], src);
-          const long long si = __shfl_sync(FULL, ci[j], src);
-          list_insert<KPL>(L, sd, si, lane);
-        }
-      }
-    } else {
-      bitonic_sort<KPL>(cd, ci, lane);
-      if (__shfl_sync(FULL, L.d[0], 0) == DINF) {  // empty list: the sorted chunk is the list
-#pragma unroll
-        for (int j = 0; j < KPL; j++) {
-          L.d[j] = cd[j];
-          L.id[j] = ci[j];
-        }
-      } else {
-        bitonic_merge_into<KPL>(L, cd, ci, lane);
-      }
-    }
-  }
-}
-
-// Per-warp scratch for the own-leaf bucket select.
-struct BucketScratch {
-  double d[64];
-  int32_t pos[64];
-  int32_t hist[32];
+// Profiling counters (MKNN_PROF=1; nullptr otherwise): what the warps did.
+enum {
+  PROF_OWN_CHUNKS_SCANNED, PROF_EXP_CHUNKS_SCANNED, PROF_INSERTS, PROF_SORT_MERGES,
+  PROF_EXP_LEAF_VISITS, PROF_OWN_CHUNKS_TOTAL, PROF_EXP_CHUNKS_TOTAL, PROF_ADMITTED, PROF_N
 };
-
-constexpr int BUCKET_EM = 12;  // candidates per lane held in registers (own leaf <= 384)
-
-__device__ __forceinline__ double warp_min(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
-  return v;
-}
-__device__ __forceinline__ double warp_max(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
-  return v;
+#ifndef MKNN_PROFILE
+#define MKNN_PROFILE 0
+#endif
+__device__ __forceinline__ void prof_add(unsigned long long* prof, int i, unsigned long long v,
+                                         int lane) {
+  if (MKNN_PROFILE && prof && lane == 0 && v) atomicAdd(&prof[i], v);
 }
 
-// histogram of bins (0..31, 32 = skip) -> first bin whose inclusive prefix
-// count reaches `need` (31 if never); *before = count strictly below it
-template <int EM>
-__device__ __forceinline__ int bucket_cut(const int (&bin)[EM], int need, int32_t* hist, int lane,
-                                          int& before) {
-  hist[lane] = 0;
-  __syncwarp();
-#pragma unroll
-  for (int i = 0; i < EM; i++)
-    if (bin[i] < 32) atomicAdd(&hist[bin[i]], 1);
-  __syncwarp();
-  const int h = hist[lane];
-  int cum = h;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int u = __shfl_up_sync(FULL, cum, o);
-    if (lane >= o) cum += u;
-  }
-  const unsigned m = __ballot_sync(FULL, cum >= need);
-  const int b = m ? __ffs(m) - 1 : 31;
-  before = __shfl_sync(FULL, cum - h, b);
-  __syncwarp();
-  return b;
-}
-
-// first_iteration for one query when the own leaf holds 33..32*EM objects
-// and k <= 32 (engine.py:356-373 with the selection of kselect.py:34-138
-// re-planned for a warp): the leaf's d2 stay in registers, a two-level
-// 32-bin histogram over [min, max] finds a cut holding >= k+1 candidates
-// (k plus room for the issuer, excluded by id afterwards), the cut is
-// compacted to shared memory and only those candidates are sorted.  The
-// binning is monotone in d2, so every candidate left out is strictly
-// farther than every candidate kept: the list is exact.
-__device__ __noinline__ void own_leaf_bucket(List<1>& L, int k, int beg, int end, double qx,
-                                             double qy, long long me,
-                                             const double2* __restrict__ xy,
-                                             const long long* __restrict__ ids, int lane,
-                                             BucketScratch* sc) {
-  constexpr int EM = BUCKET_EM;
-  double v[EM];
-  double mn = DINF, mx = -DINF;
-#pragma unroll
-  for (int i = 0; i < EM; i++) {
-    const int idx = beg + i * 32 + lane;
-    v[i] = DINF;
-    if (idx < end) {
-      const double2 p = __ldg(&xy[idx]);
-      v[i] = pair_d2(qx, qy, p.x, p.y);
+// Admit the candidates of one lane-per-candidate batch into the list.
+// cand (cd, ci) is (+inf, IDMAX) on lanes that do not pass; m = ballot of
+// passing lanes.  Few survivors are inserted one by one with warp shuffles;
+// many are sorted and merged (an empty list takes the sorted batch).
+template <int KPL>
+__device__ __forceinline__ void admit(List<KPL>& L, double cd0, long long ci0, unsigned m, int lane,
+                                      unsigned long long* prof) {
+  constexpr int INS_MAX = KPL == 1 ? 4 : 10 + 4 * KPL;
+  const int cnt = __popc(m);
+  prof_add(prof, PROF_ADMITTED, cnt, lane);
+  prof_add(prof, cnt <= INS_MAX ? PROF_INSERTS : PROF_SORT_MERGES, cnt <= INS_MAX ? cnt : 1, lane);
+  if (cnt <= INS_MAX) {
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      list_insert<KPL>(L, __shfl_sync(FULL, cd0, src), __shfl_sync(FULL, ci0, src), lane);
     }
-    if (v[i] < DINF) {
-      mn = fmin(mn, v[i]);
-      mx = fmax(mx, v[i]);
-    }
-  }
-  mn = warp_min(mn);
-  mx = warp_max(mx);
-  int total = 0;
-#pragma unroll
-  for (int i = 0; i < EM; i++) total += __popc(__ballot_sync(FULL, v[i] < DINF));
-  const int need = min(k + 1, total);
-  // level 1: 32 equal-width bins over [mn, mx]
-  const double sc1 = mx > mn ? 32.0 / (mx - mn) : 0.0;
-  int bin[EM];
-#pragma unroll
-  for (int i = 0; i < EM; i++)
-    bin[i] = v[i] < DINF ? min(31, (int)((v[i] - mn) * sc1)) : 32;
-  int before1;
-  const int b1 = bucket_cut<EM>(bin, need, sc->hist, lane, before1);
-  // level 2: 32 bins over the values of bin b1
-  double mn2 = DINF, mx2 = -DINF;
-#pragma unroll
-  for (int i = 0; i < EM; i++)
-    if (bin[i] == b1) {
-      mn2 = fmin(mn2, v[i]);
-      mx2 = fmax(mx2, v[i]);
-    }
-  mn2 = warp_min(mn2);
-  mx2 = warp_max(mx2);
-  const double sc2 = mx2 > mn2 ? 32.0 / (mx2 - mn2) : 0.0;
-  int sub[EM];
-#pragma unroll
-  for (int i = 0; i < EM; i++) sub[i] = bin[i] == b1 ? min(31, (int)((v[i] - mn2) * sc2)) : 32;
-  int before2;
-  const int b2 = bucket_cut<EM>(sub, need - before1, sc->hist, lane, before2);
-  // compact the cut into shared memory
-  const unsigned lt = (1u << lane) - 1u;
-  int c = 0;
-  bool overflow = false;
-#pragma unroll
-  for (int i = 0; i < EM; i++) {
-    const bool keep = bin[i] < b1 || (bin[i] == b1 && sub[i] <= b2);
-    const unsigned m = __ballot_sync(FULL, keep);
-    const int slot = c + __popc(m & lt);
-    if (keep && slot < 64) {
-      sc->d[slot] = v[i];
-      sc->pos[slot] = beg + i * 32 + lane;
-    }
-    c += __popc(m);
-  }
-  overflow = c > 64;
-  __syncwarp();
-  if (overflow) {  // pathological distribution (heavy ties): plain chunked pass
-    scan_range<1>(L, k, beg, end, qx, qy, me, xy, ids, lane);
     return;
   }
-  // exact (d2, id) selection among the c candidates of the cut
-  double d0 = DINF, d1 = DINF;
-  long long i0 = IDMAX, i1 = IDMAX;
-  if (lane < c) {
-    i0 = __ldg(&ids[sc->pos[lane]]);
-    d0 = i0 == me ? DINF : sc->d[lane];
-    if (i0 == me) i0 = IDMAX;
-  }
-  if (lane + 32 < c) {
-    i1 = __ldg(&ids[sc->pos[lane + 32]]);
-    d1 = i1 == me ? DINF : sc->d[lane + 32];
-    if (i1 == me) i1 = IDMAX;
-  }
-  __syncwarp();
-  double cd[1] = {d0};
-  long long ci[1] = {i0};
-  bitonic_sort<1>(cd, ci, lane);
-  L.d[0] = cd[0];
-  L.id[0] = ci[0];
-  if (c > 32) {
-    unsigned m = __ballot_sync(FULL, d1 < DINF);
-    if (__popc(m) <= 12) {
-      while (m) {
-        const int src = __ffs(m) - 1;
-        m &= m - 1;
-        list_insert<1>(L, __shfl_sync(FULL, d1, src), __shfl_sync(FULL, i1, src), lane);
+  const bool empty = __shfl_sync(FULL, L.d[0], 0) == DINF;
+  if constexpr (KPL == 1) {
+    batch_sort(cd0, ci0, lane);
+    if (empty) {  // the sorted batch is the list
+      L.d[0] = cd0;
+      L.id[0] = ci0;
+    } else {
+      merge_list(L, cd0, ci0, lane);
+    }
+  } else {
+    double bd[1] = {cd0};
+    long long bi[1] = {ci0};
+    bitonic_sort<1>(bd, bi, lane);
+    double cd[KPL];
+    long long ci[KPL];
+    cd[0] = bd[0];
+    ci[0] = bi[0];
+#pragma unroll
+    for (int s = 1; s < KPL; s++) {
+      cd[s] = DINF;
+      ci[s] = IDMAX;
+    }
+    if (empty) {
+#pragma unroll
+      for (int s = 0; s < KPL; s++) {
+        L.d[s] = cd[s];
+        L.id[s] = ci[s];
       }
     } else {
-      cd[0] = d1;
-      ci[0] = i1;
-      bitonic_sort<1>(cd, ci, lane);
-      bitonic_merge_into<1>(L, cd, ci, lane);
+      bitonic_merge_into<KPL>(L, cd, ci, lane);
+    }
+  }
+}
+
+// engine.py:279-324 _merge_pack for one row restricted to one chunk of a
+// leaf: every object of [beg, end) (<= 32) except the issuer (by id,
+// engine.py:298-300) competes for the list; admission is (d2, id) < k-th.
+template <int KPL>
+__device__ __forceinline__ bool scan_chunk(List<KPL>& L, double kd, long long ki, int beg, int end,
+                                           double qx, double qy, long long me,
+                                           const StoreRec* __restrict__ obj, int lane,
+                                           unsigned long long* prof) {
+  const int idx = beg + lane;
+  bool pass = false;
+  double d2 = DINF;
+  long long id = IDMAX;
+  if (idx < end) {
+    const double2 p = obj_xy(obj, idx);
+    d2 = pair_d2(qx, qy, p.x, p.y);
+    if (d2 <= kd) {
+      id = obj_id(obj, idx);
+      pass = (id != me) && key_less(d2, id, kd, ki);
+    }
+  }
+  const unsigned m = __ballot_sync(FULL, pass);
+  if (m) admit<KPL>(L, pass ? d2 : DINF, pass ? id : IDMAX, m, lane, prof);
+  return m != 0;
+}
+
+// min-dist2 from the query to a chunk's point bounding box: a lower bound of
+// pair_d2 for every object of the chunk (each step is a correctly rounded,
+// monotone operation of the same inputs pair_d2 rounds; geometry.py:189-193)
+__device__ __forceinline__ double mindist2_box(const ChunkBox& b, double qx, double qy) {
+  const double dx = fmax(fmax(__dsub_rn(b.x_lo, qx), __dsub_rn(qx, b.x_hi)), 0.0);
+  const double dy = fmax(fmax(__dsub_rn(b.y_lo, qy), __dsub_rn(qy, b.y_hi)), 0.0);
+  return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+}
+
+// One row of the reference's distance phase (first_iteration's own leaf,
+// engine.py:356-373, or update_nn_lists' assigned leaf, 376-393): every
+// object of the leaf competes for the list.  Chunks whose box min-dist2
+// exceeds the current k-th d2 cannot hold an admissible object (admission
+// needs d2 <= k-th) and are skipped without changing the result; the others
+// are visited nearest box first, so the list tightens early.
+template <int KPL>
+__device__ __forceinline__ void visit_leaf(List<KPL>& L, int k, int leaf, double qx, double qy,
+                                           long long me, const SearchArgs& a, int lane, bool own) {
+  const int ob = __ldg(&a.cell_start[leaf]), oe = __ldg(&a.cell_start[leaf + 1]);
+  const int c0 = __ldg(&a.chunk_start[leaf]), c1 = __ldg(&a.chunk_start[leaf + 1]);
+  prof_add(a.prof, own ? PROF_OWN_CHUNKS_TOTAL : PROF_EXP_CHUNKS_TOTAL, c1 - c0, lane);
+  if (!own) prof_add(a.prof, PROF_EXP_LEAF_VISITS, 1, lane);
+  double kd;
+  long long ki;
+  list_kth<KPL>(L, k, kd, ki);
+  for (int g = c0; g < c1; g += 32) {
+    bool live = g + lane < c1;
+    double md = DINF;
+    if (live) md = mindist2_box(a.box[g + lane], qx, qy);
+    for (;;) {
+      const bool cand = live && md <= kd;
+      if (!__any_sync(FULL, cand)) break;
+      // nearest box first (approximate key: md rounded down to float, lane
+      // in the low bits); the visit order only affects speed
+      const unsigned key =
+          cand ? ((__float_as_uint(__double2float_rd(md)) & ~31u) | (unsigned)lane) : 0xffffffffu;
+      const int src = (int)(__reduce_min_sync(FULL, key) & 31u);
+      if (lane == src) live = false;
+      const int cb = ob + (g - c0 + src) * CHUNK;
+      prof_add(a.prof, own ? PROF_OWN_CHUNKS_SCANNED : PROF_EXP_CHUNKS_SCANNED, 1, lane);
+      if (scan_chunk<KPL>(L, kd, ki, cb, min(cb + CHUNK, oe), qx, qy, me, a.obj, lane, a.prof))
+        list_kth<KPL>(L, k, kd, ki);
     }
   }
 }
@@ -404,8 +408,7 @@ __device__ __forceinline__ void emit_task(const SearchArgs& a, unsigned dir, uin
 // does it hold an object (not the issuer) strictly closer than thr?
 __device__ __noinline__ bool audit_quadrant(const int32_t* __restrict__ z_map,
                                             const int32_t* __restrict__ cell_start,
-                                            const double2* __restrict__ xy,
-                                            const long long* __restrict__ ids, Region r, int l_deep,
+                                            const StoreRec* __restrict__ obj, Region r, int l_deep,
                                             int lvl, long long qc, double thr, double qx, double qy,
                                             long long me) {
   const int sh = 2 * (l_deep - lvl);
@@ -414,9 +417,9 @@ __device__ __noinline__ bool audit_quadrant(const int32_t* __restrict__ z_map,
   for (int li = l0; li <= l1; li++) {
     const int b = cell_start[li], e = cell_start[li + 1];
     for (int i = b; i < e; i++) {
-      const double2 p = xy[i];
+      const StoreRec& p = obj[i];
       const long long c = encode(p.x, p.y, r, l_deep);
-      if (c >= lo && c < hi && ids[i] != me && pair_d2(qx, qy, p.x, p.y) < thr) return true;
+      if (c >= lo && c < hi && p.id != me && pair_d2(qx, qy, p.x, p.y) < thr) return true;
     }
   }
   return false;
@@ -440,7 +443,7 @@ __device__ __forceinline__ int navigate(const SearchArgs& a, int l_deep, int dir
     const double md2 = full ? mindist2_cell(lvl, qc, a.r, qx, qy) : 0.0;
     if (md2 > thr) {  // prune (engine.py:447-460; strict, see the header)
       prunes++;
-      if (a.audit && audit_quadrant(a.z_map, a.cell_start, a.xy, a.ids, a.r, l_deep, lvl, qc, thr,
+      if (a.audit && audit_quadrant(a.z_map, a.cell_start, a.obj, a.r, l_deep, lvl, qc, thr,
                                     qx, qy, me))
         viol++;
       pos += sign << (2 * delta);
@@ -489,17 +492,14 @@ __device__ __forceinline__ void list_store(const List<KPL>& L, double* __restric
 // lists live in shared memory between steps; leaf scans are warp-wide
 // (32 candidates per ballot), navigation is lane-parallel (lane q walks
 // query q), mirroring the paper's thread-per-query navigation.
-template <int KPL, int B>
-__global__ void __launch_bounds__(32 * WARPS_PER_CTA) k_search(const SearchArgs a) {
+template <int KPL, int B, int WARPS, int MINB>
+__global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a) {
   constexpr int N = 32 * KPL;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double* sd = reinterpret_cast<double*>(smem_raw) + (size_t)w * B * N;
-  long long* si = reinterpret_cast<long long*>(smem_raw) + (size_t)WARPS_PER_CTA * B * N +
-                  (size_t)w * B * N;
-  BucketScratch* bsc = reinterpret_cast<BucketScratch*>(
-                          smem_raw + (size_t)WARPS_PER_CTA * B * N * 16) + w;
-  const int64_t t0 = ((int64_t)blockIdx.x * WARPS_PER_CTA + w) * B;
+  long long* si = reinterpret_cast<long long*>(smem_raw) + (size_t)WARPS * B * N + (size_t)w * B * N;
+  const int64_t t0 = ((int64_t)blockIdx.x * WARPS + w) * B;
   if (t0 >= a.nq) return;
   const int nb = (int)((a.nq - t0) < B ? (a.nq - t0) : B);
   const int l_deep = __ldg(&a.scalars[0]);
@@ -521,7 +521,9 @@ __global__ void __launch_bounds__(32 * WARPS_PER_CTA) k_search(const SearchArgs 
     cur_l = (long long)__ldg(&a.leaf_key[own]) - 1;
     cur_r = (long long)__ldg(&a.leaf_key[own]) + (long long)__ldg(&a.leaf_span[own]);
     act_l = act_r = true;
-    if (__ldg(&a.cell_start[own + 1]) > __ldg(&a.cell_start[own])) emit_task(a, 0, 0, own);
+    const int pop = __ldg(&a.cell_start[own + 1]) - __ldg(&a.cell_start[own]);
+    evals = (uint32_t)pop;  // first_iteration row (rows with 0 candidates dropped, engine.py:334-338)
+    if (pop > 0) emit_task(a, 0, 0, own);
   }
 
   // first_iteration: every query against its own leaf
@@ -535,21 +537,7 @@ __global__ void __launch_bounds__(32 * WARPS_PER_CTA) k_search(const SearchArgs 
       L.d[s] = DINF;
       L.id[s] = IDMAX;
     }
-    const int b = __ldg(&a.cell_start[jown]), e = __ldg(&a.cell_start[jown + 1]);
-    if (e > b) {  // rows with 0 candidates are dropped (engine.py:334-338)
-      if constexpr (KPL == 1) {
-        if (e - b > 32) {
-          const int cut = min(e, b + 32 * BUCKET_EM);
-          own_leaf_bucket(L, k, b, cut, jx, jy, jme, a.xy, a.ids, lane, bsc);
-          if (cut < e) scan_range<KPL>(L, k, cut, e, jx, jy, jme, a.xy, a.ids, lane);
-        } else {
-          scan_range<KPL>(L, k, b, e, jx, jy, jme, a.xy, a.ids, lane);
-        }
-      } else {
-        scan_range<KPL>(L, k, b, e, jx, jy, jme, a.xy, a.ids, lane);
-      }
-      if (lane == j) evals += (uint32_t)(e - b);
-    }
+    visit_leaf<KPL>(L, k, (int)jown, jx, jy, jme, a, lane, true);
     double kd;
     long long ki;
     list_kth<KPL>(L, k, kd, ki);
@@ -576,7 +564,10 @@ __global__ void __launch_bounds__(32 * WARPS_PER_CTA) k_search(const SearchArgs 
         cur_l = cur;
         act_l = li >= 0;
       }
-      if (li >= 0) emit_task(a, go_right ? 2 : 1, (go_right ? calls_r : calls_l) - 1, li);
+      if (li >= 0) {
+        emit_task(a, go_right ? 2 : 1, (go_right ? calls_r : calls_l) - 1, li);
+        evals += (uint32_t)(__ldg(&a.cell_start[li + 1]) - __ldg(&a.cell_start[li]));
+      }
     }
     // update_nn_lists: merge each assigned leaf into its query's list
     unsigned pend = __ballot_sync(FULL, li >= 0);
@@ -586,18 +577,14 @@ __global__ void __launch_bounds__(32 * WARPS_PER_CTA) k_search(const SearchArgs 
       const int jl = __shfl_sync(FULL, li, j);
       const double jx = __shfl_sync(FULL, qx, j), jy = __shfl_sync(FULL, qy, j);
       const long long jme = __shfl_sync(FULL, me, j);
-      const int b = __ldg(&a.cell_start[jl]), e = __ldg(&a.cell_start[jl + 1]);
       List<KPL> L;
       list_load<KPL>(L, sd + j * N, si + j * N, lane);
-      scan_range<KPL>(L, k, b, e, jx, jy, jme, a.xy, a.ids, lane);
+      visit_leaf<KPL>(L, k, jl, jx, jy, jme, a, lane, false);
       list_store<KPL>(L, sd + j * N, si + j * N, lane);
       double kd;
       long long ki;
       list_kth<KPL>(L, k, kd, ki);
-      if (lane == j) {
-        thr = kd;
-        evals += (uint32_t)(e - b);
-      }
+      if (lane == j) thr = kd;
     }
     __syncwarp();
     go_right = !go_right;
@@ -630,227 +617,6 @@ __global__ void __launch_bounds__(32 * WARPS_PER_CTA) k_search(const SearchArgs 
     st.nav_right = (uint16_t)min(calls_r, 65535u);
     st.violations = viol;
     a.stats[t0 + lane] = st;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Thread-per-query search for k <= 32 (the paper's distComp mapping, "CTA
-// per leaf, thread per query", re-planned for one warp):
-// lane q owns query t0+q of the leaf-grouped order, so the lanes of a warp
-// mostly read the same leaf objects (broadcast loads).  Each query keeps its
-// k best (d2, id) UNSORTED in shared memory with the current maximum (the
-// k-th neighbour) cached in registers; it is sorted once, at emission.
-//
-// Own leaf: two passes.  Pass A histograms the query's candidates into 64
-// monotone log-spaced bins of t = d2 / R2 (R2 = squared leaf diagonal;
-// float exponent + 2 mantissa bits); the first bin whose prefix count
-// reaches k+1 (k plus room for the issuer) is the cut.  Pass B offers only
-// candidates at or below the cut.  Binning is monotone in d2, so everything
-// above the cut is strictly farther than everything kept: exact.
-constexpr int TPQ_WARPS = 4;
-constexpr int TPQ_BINS = 64;
-constexpr int TPQ_STRIDE = 33;  // padded slot stride: conflict-free rows and columns
-
-struct TpqList {
-  double* d;     // [slot * 33 + lane]
-  long long* id;
-  int k, cnt, kpos;
-  double kd;
-  long long ki;
-};
-
-__device__ __forceinline__ void tpq_find_max(TpqList& L, int lane) {
-  L.kd = -1.0;
-  L.ki = -1;
-  L.kpos = 0;
-  for (int s = 0; s < L.k; s++) {
-    const double d = L.d[s * TPQ_STRIDE + lane];
-    const long long i = L.id[s * TPQ_STRIDE + lane];
-    if (key_less(L.kd, L.ki, d, i)) {
-      L.kd = d;
-      L.ki = i;
-      L.kpos = s;
-    }
-  }
-}
-
-// offer (d2, id) to the list (caller guarantees d2 < +inf and id != issuer)
-__device__ __forceinline__ void tpq_offer(TpqList& L, double d2, long long id, int lane) {
-  if (L.cnt < L.k) {
-    L.d[L.cnt * TPQ_STRIDE + lane] = d2;
-    L.id[L.cnt * TPQ_STRIDE + lane] = id;
-    if (++L.cnt == L.k) tpq_find_max(L, lane);
-  } else if (key_less(d2, id, L.kd, L.ki)) {
-    L.d[L.kpos * TPQ_STRIDE + lane] = d2;
-    L.id[L.kpos * TPQ_STRIDE + lane] = id;
-    tpq_find_max(L, lane);
-  }
-}
-
-// the k-th neighbour's d2 while the list is full, +inf before (engine.py:415)
-__device__ __forceinline__ double tpq_thr(const TpqList& L) { return L.cnt == L.k ? L.kd : DINF; }
-
-__device__ __forceinline__ int tpq_bin(double d2, double inv_r2) {
-  const float t = (float)(d2 * inv_r2);
-  const int key = (int)(__float_as_uint(t) >> 21) - ((127 - 16) << 2);
-  return min(max(key, 0), TPQ_BINS - 1);
-}
-
-// merge one leaf [b, e) into the list (update_nn_lists, engine.py:376-393)
-__device__ __forceinline__ void tpq_scan(TpqList& L, int b, int e, double qx, double qy,
-                                         long long me, const double2* __restrict__ xy,
-                                         const long long* __restrict__ ids, int lane) {
-  for (int j = b; j < e; j++) {
-    const double2 p = __ldg(&xy[j]);
-    const double d2 = pair_d2(qx, qy, p.x, p.y);
-    if (d2 <= tpq_thr(L) && d2 < DINF) {
-      const long long id = __ldg(&ids[j]);
-      if (id != me) tpq_offer(L, d2, id, lane);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(32 * TPQ_WARPS) k_search_tpq(const SearchArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int k = a.k;
-  const size_t per_warp = (size_t)max(k * TPQ_STRIDE * 16, TPQ_BINS * 32 * 4);
-  unsigned char* base = smem_raw + (size_t)w * per_warp;
-  const int64_t t = ((int64_t)blockIdx.x * TPQ_WARPS + w) * 32 + lane;
-  if (((int64_t)blockIdx.x * TPQ_WARPS + w) * 32 >= a.nq) return;
-  const bool mine = t < a.nq;
-  const int l_deep = __ldg(&a.scalars[0]);
-
-  TpqList L;
-  L.d = reinterpret_cast<double*>(base);
-  L.id = reinterpret_cast<long long*>(base + (size_t)k * TPQ_STRIDE * 8);
-  L.k = k;
-  L.cnt = 0;
-  L.kpos = 0;
-  L.kd = DINF;
-  L.ki = IDMAX;
-  uint32_t* hist = reinterpret_cast<uint32_t*>(base);  // aliases the list during pass A
-
-  uint32_t q = 0, own = 0;
-  double qx = 0.0, qy = 0.0;
-  long long me = 0, cur_l = -1, cur_r = 0;
-  uint32_t evals = 0, prunes = 0, viol = 0, calls_l = 0, calls_r = 0;
-  bool act_l = false, act_r = false;
-  int ob = 0, oe = 0;
-  if (mine) {
-    q = __ldg(&a.q_order[t]);
-    qx = __ldg(&a.qx[q]);
-    qy = __ldg(&a.qy[q]);
-    me = __ldg(&a.qi[q]);
-    own = __ldg(&a.q_leaf[q]);
-    const long long key = __ldg(&a.leaf_key[own]);
-    cur_l = key - 1;
-    cur_r = key + (long long)__ldg(&a.leaf_span[own]);
-    act_l = act_r = true;
-    ob = __ldg(&a.cell_start[own]);
-    oe = __ldg(&a.cell_start[own + 1]);
-    evals = (uint32_t)(oe - ob);  // first_iteration row (0 when the leaf is empty)
-    if (oe > ob) emit_task(a, 0, 0, own);
-  }
-
-  // ---- first_iteration: own leaf, pass A (histogram) --------------------
-  const int n_own = oe - ob;
-  int cut = TPQ_BINS - 1;
-  double inv_r2 = 0.0;
-  if (n_own > k + 1) {
-    // R2 = squared diagonal of the own leaf's quadrant (scale only)
-    const int lvl = l_deep - ((31 - __clz(__ldg(&a.leaf_span[own]))) >> 1);
-    const double lw = a.r.w * pow2_neg(lvl), lh = a.r.h * pow2_neg(lvl);
-    const double r2 = lw * lw + lh * lh;
-    inv_r2 = r2 > 0.0 ? 1.0 / r2 : 0.0;
-#pragma unroll 4
-    for (int bI = 0; bI < TPQ_BINS; bI++) hist[bI * 32 + lane] = 0;
-    for (int j = ob; j < oe; j++) {
-      const double2 p = __ldg(&a.xy[j]);
-      const int bI = tpq_bin(pair_d2(qx, qy, p.x, p.y), inv_r2);
-      hist[bI * 32 + lane] += 1;
-    }
-    uint32_t cum = 0;
-    for (cut = 0; cut < TPQ_BINS - 1; cut++) {
-      cum += hist[cut * 32 + lane];
-      if (cum >= (uint32_t)(k + 1)) break;
-    }
-  }
-  __syncwarp();
-  // ---- pass B: offer the candidates at or below the cut ------------------
-  for (int j = ob; j < oe; j++) {
-    const double2 p = __ldg(&a.xy[j]);
-    const double d2 = pair_d2(qx, qy, p.x, p.y);
-    if (d2 < DINF && (cut == TPQ_BINS - 1 || tpq_bin(d2, inv_r2) <= cut) && d2 <= tpq_thr(L)) {
-      const long long id = __ldg(&a.ids[j]);
-      if (id != me) tpq_offer(L, d2, id, lane);
-    }
-  }
-
-  // ---- direction loop, left first (engine.py:645-681) ---------------------
-  bool go_right = false;
-  if (a.debug_phase == 1) act_l = act_r = false;
-  while (__any_sync(FULL, act_l || act_r)) {
-    const bool act = go_right ? act_r : act_l;
-    if (act) {
-      long long cur = go_right ? cur_r : cur_l;
-      const int li = navigate(a, l_deep, go_right ? 1 : 0, cur, tpq_thr(L), qx, qy, me, prunes, viol);
-      if (go_right) {
-        calls_r++;
-        cur_r = cur;
-        act_r = li >= 0;
-      } else {
-        calls_l++;
-        cur_l = cur;
-        act_l = li >= 0;
-      }
-      if (li >= 0) {
-        emit_task(a, go_right ? 2 : 1, (go_right ? calls_r : calls_l) - 1, li);
-        const int b = __ldg(&a.cell_start[li]), e = __ldg(&a.cell_start[li + 1]);
-        evals += (uint32_t)(e - b);
-        tpq_scan(L, b, e, qx, qy, me, a.xy, a.ids, lane);
-      }
-    }
-    go_right = !go_right;
-  }
-
-  // ---- _emit: sort each list by (d2, id), then write rows warp-wide ------
-  for (int i = 1; i < L.cnt; i++) {
-    const double d = L.d[i * TPQ_STRIDE + lane];
-    const long long id = L.id[i * TPQ_STRIDE + lane];
-    int p = i;
-    while (p > 0) {
-      const double pd = L.d[(p - 1) * TPQ_STRIDE + lane];
-      const long long pi = L.id[(p - 1) * TPQ_STRIDE + lane];
-      if (!key_less(d, id, pd, pi)) break;
-      L.d[p * TPQ_STRIDE + lane] = pd;
-      L.id[p * TPQ_STRIDE + lane] = pi;
-      p--;
-    }
-    L.d[p * TPQ_STRIDE + lane] = d;
-    L.id[p * TPQ_STRIDE + lane] = id;
-  }
-  __syncwarp();
-  const int64_t rem = a.nq - (t - lane);
-  const int nb = rem < 32 ? (int)rem : 32;
-  const uint32_t my_row = mine ? __ldg(&a.q_row[q]) : 0;
-  for (int j = 0; j < nb; j++) {
-    const uint32_t row = __shfl_sync(FULL, my_row, j);
-    const int cnt = __shfl_sync(FULL, L.cnt, j);
-    if (lane < cnt) {
-      a.out_nids[(int64_t)row * k + lane] = L.id[lane * TPQ_STRIDE + j];
-      a.out_dist[(int64_t)row * k + lane] = __dsqrt_rn(L.d[lane * TPQ_STRIDE + j]);
-    }
-    if (lane == 0) a.out_len[row] = cnt;
-  }
-  if (mine) {
-    QueryStats st;
-    st.evals = evals;
-    st.prunes = prunes;
-    st.nav_left = (uint16_t)min(calls_l, 65535u);
-    st.nav_right = (uint16_t)min(calls_r, 65535u);
-    st.violations = viol;
-    a.stats[t] = st;
   }
 }
 
@@ -892,11 +658,29 @@ __global__ void k_stats_reduce(const QueryStats* __restrict__ st, int64_t nq,
   }
 }
 
+// The search writes padded rows (k slots each) straight into the caller's
+// output; that IS the CSR layout when every row is full (min(k, objects
+// other than the issuer) == k, the common case).  Otherwise the rows are
+// moved to `tmp` and compacted back.  Both kernels read the CSR total on the
+// device and return at once when every row is full (no host round trip).
+__global__ void k_rows_stash(const int64_t* __restrict__ off, int64_t nq, int k,
+                             const long long* __restrict__ nids, const double* __restrict__ dist,
+                             long long* __restrict__ t_nids, double* __restrict__ t_dist) {
+  const int64_t total = nq * (int64_t)k;
+  if (off[nq] == total) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    t_nids[i] = nids[i];
+    t_dist[i] = dist[i];
+  }
+}
+
 __global__ void k_rows_compact(const int32_t* __restrict__ len, const long long* __restrict__ nids,
                                const double* __restrict__ dist, int64_t nq, int k,
                                const int64_t* __restrict__ off, long long* __restrict__ c_nids,
                                double* __restrict__ c_dist) {
   const int64_t total = nq * (int64_t)k;
+  if (off[nq] == total) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / k;
@@ -910,48 +694,32 @@ __global__ void k_rows_compact(const int32_t* __restrict__ len, const long long*
 
 }  // namespace
 
-template <int KPL, int B>
+template <int KPL, int B, int WARPS, int MINB = 1>
 int launch_batched(const SearchArgs& a, cudaStream_t s) {
   constexpr int N = 32 * KPL;
-  const size_t smem = (size_t)WARPS_PER_CTA * B * N * (sizeof(double) + sizeof(long long)) +
-                      (size_t)WARPS_PER_CTA * sizeof(BucketScratch);
+  const size_t smem = (size_t)WARPS * B * N * (sizeof(double) + sizeof(long long));
   static bool configured = false;
   if (!configured) {
-    MKNN_CUDA_OK(cudaFuncSetAttribute(k_search<KPL, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
+    MKNN_CUDA_OK(cudaFuncSetAttribute(k_search<KPL, B, WARPS, MINB>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
-  const int64_t per_cta = (int64_t)WARPS_PER_CTA * B;
+  const int64_t per_cta = (int64_t)WARPS * B;
   const unsigned blocks = (unsigned)((a.nq + per_cta - 1) / per_cta);
-  MKNN_LAUNCH k_search<KPL, B><<<blocks, 32 * WARPS_PER_CTA, smem, s>>>(a);
-  MKNN_CUDA_OK(cudaGetLastError());
-  return 0;
-}
-
-int launch_tpq(const SearchArgs& a, cudaStream_t s) {
-  const size_t per_warp = (size_t)std::max(a.k * TPQ_STRIDE * 16, TPQ_BINS * 32 * 4);
-  const size_t smem = per_warp * TPQ_WARPS;
-  static size_t configured = 0;
-  if (smem > configured) {
-    MKNN_CUDA_OK(cudaFuncSetAttribute(k_search_tpq, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-    configured = smem;
-  }
-  const int64_t per_cta = (int64_t)TPQ_WARPS * 32;
-  const unsigned blocks = (unsigned)((a.nq + per_cta - 1) / per_cta);
-  MKNN_LAUNCH k_search_tpq<<<blocks, 32 * TPQ_WARPS, smem, s>>>(a);
+  MKNN_LAUNCH k_search<KPL, B, WARPS, MINB><<<blocks, 32 * WARPS, smem, s>>>(a);
   MKNN_CUDA_OK(cudaGetLastError());
   return 0;
 }
 
 int search_launch(const SearchArgs& a, cudaStream_t s) {
   if (a.nq == 0) return 0;
-  if (a.k <= 32 && !a.force_warp) return launch_tpq(a, s);
-  if (a.k <= 32) return launch_batched<1, 16>(a, s);
-  if (a.k <= 64) return launch_batched<2, 8>(a, s);
-  if (a.k <= 128) return launch_batched<4, 4>(a, s);
-  if (a.k <= 256) return launch_batched<8, 2>(a, s);
-  if (a.k <= 512) return launch_batched<16, 1>(a, s);
+  // k <= 32: 16 queries per warp, 4 warps per CTA, <= 80 registers: the
+  // occupancy/latency optimum measured on B200
+  if (a.k <= 32) return launch_batched<1, 16, 4, 6>(a, s);
+  if (a.k <= 64) return launch_batched<2, 16, 4>(a, s);
+  if (a.k <= 128) return launch_batched<4, 8, 4>(a, s);
+  if (a.k <= 256) return launch_batched<8, 4, 4>(a, s);
+  if (a.k <= 512) return launch_batched<16, 2, 4>(a, s);
   return fail_msg(E_UNSUPPORTED, "k > 512 is not supported by the device top-k");
 }
 
@@ -965,15 +733,17 @@ int stats_reduce(const QueryStats* st, int64_t nq, unsigned long long* dev_tot, 
   return 0;
 }
 
-int rows_compact(const int32_t* len, const long long* nids, const double* dist, int64_t nq, int k,
-                 int64_t* offsets, long long* c_nids, double* c_dist, void* scratch,
+int rows_compact(const int32_t* len, long long* nids, double* dist, int64_t nq, int k,
+                 int64_t* offsets, long long* t_nids, double* t_dist, void* scratch,
                  cudaStream_t s) {
   int rc = exclusive_scan_i32_to_i64(len, offsets, nq, scratch, s);
   if (rc) return rc;
   if (nq == 0) return 0;
   const int64_t total = nq * (int64_t)k;
-  int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
-  MKNN_LAUNCH k_rows_compact<<<(unsigned)blocks, 256, 0, s>>>(len, nids, dist, nq, k, offsets, c_nids, c_dist);
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
+  MKNN_LAUNCH k_rows_stash<<<(unsigned)blocks, 256, 0, s>>>(offsets, nq, k, nids, dist, t_nids, t_dist);
+  MKNN_LAUNCH k_rows_compact<<<(unsigned)blocks, 256, 0, s>>>(len, t_nids, t_dist, nq, k, offsets, nids,
+                                                             dist);
   MKNN_CUDA_OK(cudaGetLastError());
   return 0;
 }
