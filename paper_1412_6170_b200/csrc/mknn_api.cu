@@ -168,7 +168,9 @@ struct mknn_engine {
 
   DevIndex ix;
   bool have_index = false;
-  bool last_tick_ok = false;  // false: the store's sub-cell counters may be dirty
+  bool last_tick_ok = false;
+  int issuer_bits = -1;        // issuer-id bits of the last tick (plans the row sort)
+  bool retry_rebuild = false;  // false: the store's sub-cell counters may be dirty
   int32_t h_l_deep = 0;
   int64_t h_n_leaves = 0, h_overfull = 0, h_n_build = 0, h_n_sub = 0;
   DevStore st;
@@ -306,9 +308,11 @@ int refresh_index_info(mknn_engine* h) {
 }
 
 // Engine.process_tick over device-resident inputs; results into `o`.
-int core_tick(mknn_engine* h, int64_t n, const long long* ids, const double* x, const double* y,
-              int64_t nq, const long long* qi, const double* qx, const double* qy, const DevOut& o,
-              mknn_metrics* met, std::chrono::steady_clock::time_point t_start) {
+int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double* x,
+                   const double* y, int64_t nq, const long long* qi, const double* qx,
+                   const double* qy, const DevOut& o, mknn_metrics* met,
+                   std::chrono::steady_clock::time_point t_start, bool force_rebuild, bool* retry) {
+  *retry = false;
   const int k = h->cfg.k;
   cudaStream_t s = h->stream;
   int rc;
@@ -335,8 +339,8 @@ int core_tick(mknn_engine* h, int64_t n, const long long* ids, const double* x, 
   m.n_queries = nq;
 
   MKNN_CUDA_OK(cudaEventRecord(h->ev[0], s));
-  const bool rebuild =
-      !h->have_index || should_rebuild(h->history, h->cfg.rebuild_window, h->cfg.rebuild_factor);
+  const bool rebuild = force_rebuild || !h->have_index ||
+                       should_rebuild(h->history, h->cfg.rebuild_window, h->cfg.rebuild_factor);
   if (rebuild) {
     if ((rc = index_build(h->ix, h->r, x, y, n, h->scratch.p, s))) return h->set_err(rc);
     h->have_index = true;
@@ -352,8 +356,9 @@ int core_tick(mknn_engine* h, int64_t n, const long long* ids, const double* x, 
                                 h->counters + 3, h->scratch.p, s)))
     return h->set_err(rc);
   MKNN_CUDA_OK(cudaEventRecord(h->ev[2], s));
-  if ((rc = queries_index(h->dq, h->st, h->ix, h->r, qi, qx, qy, nq, h->h_n_sub, o.qids,
-                          h->scratch.p, s)))
+  int bits_used = 0;
+  if ((rc = queries_index(h->dq, h->st, h->ix, h->r, qi, qx, qy, nq, h->h_n_sub, h->issuer_bits,
+                          &bits_used, o.qids, h->scratch.p, s)))
     return h->set_err(rc);
   MKNN_CUDA_OK(cudaEventRecord(h->ev[3], s));
 
@@ -438,9 +443,22 @@ int core_tick(mknn_engine* h, int64_t n, const long long* ids, const double* x, 
 
   unsigned long long cnt[8];
   MKNN_CUDA_OK(cudaMemcpyAsync(cnt, h->counters, sizeof(cnt), cudaMemcpyDeviceToHost, s));
+  int64_t mm[2] = {0, 0};
+  if (nq) MKNN_CUDA_OK(cudaMemcpyAsync(mm, h->dq.minmax, sizeof(mm), cudaMemcpyDeviceToHost, s));
   int64_t total = 0;
   MKNN_CUDA_OK(cudaMemcpyAsync(&total, o.offsets + nq, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   MKNN_CUDA_OK(cudaStreamSynchronize(s));
+  if (nq) {
+    // the issuer sort was planned from the previous tick's id range: if this
+    // tick's range needs more bits the row order is wrong -> redo the tick
+    const int need = issuer_bits(mm[0], mm[1]);
+    h->issuer_bits = need;
+    if (need > bits_used) {
+      *retry = true;
+      h->retry_rebuild = rebuild;
+      return 0;
+    }
+  }
 
   // engine.py:661-663 active lists from navigate-call histograms
   for (int d = 0; d < 2; d++) {
@@ -498,6 +516,18 @@ int core_tick(mknn_engine* h, int64_t n, const long long* ids, const double* x, 
   }
   if (met) *met = m;
   return 0;
+}
+
+int core_tick(mknn_engine* h, int64_t n, const long long* ids, const double* x, const double* y,
+              int64_t nq, const long long* qi, const double* qx, const double* qy, const DevOut& o,
+              mknn_metrics* met, std::chrono::steady_clock::time_point t_start) {
+  bool retry = false;
+  int rc = core_tick_once(h, n, ids, x, y, nq, qi, qx, qy, o, met, t_start, false, &retry);
+  if (rc || !retry) return rc;
+  // issuer bits now measured exactly: the second pass cannot retry
+  rc = core_tick_once(h, n, ids, x, y, nq, qi, qx, qy, o, met, t_start, h->retry_rebuild, &retry);
+  if (!rc && retry) return fail_msg(E_CUDA, "issuer order retry did not converge");
+  return rc;
 }
 
 int validate_counts(mknn_engine* h, int64_t n, int64_t nq) {
@@ -696,7 +726,11 @@ int mknn_create(const mknn_config* cfg, mknn_engine** out) {
   auto* h = new mknn_engine();
   h->cfg = *cfg;
   h->device = cfg->device;
-  h->r = Region{cfg->x_lo, cfg->y_lo, cfg->x_hi, cfg->y_hi, cfg->x_hi - cfg->x_lo, cfg->y_hi - cfg->y_lo};
+  {
+    const double w = cfg->x_hi - cfg->x_lo, hh = cfg->y_hi - cfg->y_lo;
+    h->r = Region{cfg->x_lo, cfg->y_lo, cfg->x_hi, cfg->y_hi, w, hh, w > 0.0 ? 1.0 / w : 0.0,
+                  hh > 0.0 ? 1.0 / hh : 0.0};
+  }
   int rc = bind(h);
   if (!rc) rc = index_alloc(h->ix, cfg->l_max, cfg->th_quad);
   if (!rc && cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking) != cudaSuccess) rc = E_CUDA;

@@ -19,6 +19,7 @@ constexpr int MAX_L_MAX = 10;  // quadindex.py:20
 struct Region {
   double x_lo, y_lo, x_hi, y_hi;
   double w, h;  // x_hi - x_lo, y_hi - y_lo computed on the host (geometry.py:46-52)
+  double inv_w, inv_h;  // 1 / w, 1 / h (0 when the width is 0): fast path of coord16
 };
 
 // offset of level l in the concatenated count pyramid (levels 0..l_max);
@@ -77,12 +78,41 @@ __device__ __forceinline__ uint32_t cell_coord(double v, double lo, double width
   return (uint32_t)c;
 }
 
+// cell coordinate of one axis at level 16, exactly
+//   clip(floor(fl((v - lo) / width) * 2^16), 0, 2^16 - 1)   (geometry.py:105-129)
+// The quotient is first formed with the reciprocal (two roundings, so it is
+// within 2^-51 relative of the IEEE quotient); only when the scaled value
+// lands within 2^-30 of a cell border -- where the two quotients could floor
+// differently -- is the IEEE division evaluated.  Coarser levels L are the
+// prefixes c16 >> (16 - L) (the same t at every level, geometry.py:108-112).
+__device__ __forceinline__ uint32_t coord16(double v, double lo, double width, double inv_width) {
+  if (!(width > 0.0)) return 0;
+  const double d = __dsub_rn(v, lo);
+  const double f = __dmul_rn(__dmul_rn(d, inv_width), 65536.0);
+  double c = floor(f);
+  const double fr = __dsub_rn(f, c);  // exact
+  if (fr < 0x1p-30 || fr > 1.0 - 0x1p-30) c = floor(__dmul_rn(__ddiv_rn(d, width), 65536.0));
+  c = fmax(c, 0.0);
+  c = fmin(c, 65535.0);
+  return (uint32_t)c;
+}
+
+// Morton code at level 16 of a point (x bits even, y bits odd)
+__device__ __forceinline__ uint32_t encode16(double x, double y, const Region& r) {
+  return spread_bits32(coord16(x, r.x_lo, r.w, r.inv_w)) |
+         (spread_bits32(coord16(y, r.y_lo, r.h, r.inv_h)) << 1);
+}
+
 // geometry.py:132-135 encode_points (x bits even, y bits odd; SW,SE,NW,NE)
 __device__ __forceinline__ uint32_t encode(double x, double y, const Region& r, int level) {
   const uint32_t cx = cell_coord(x, r.x_lo, r.w, level);
   const uint32_t cy = cell_coord(y, r.y_lo, r.h, level);
   return spread_bits32(cx) | (spread_bits32(cy) << 1);
 }
+
+// max(a, b) without NaN handling (coordinates are finite; the reference's
+// np.maximum only differs on NaN)
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
 
 // geometry.py:166-181 cell_bounds_arrays + 189-193 min_dist2_point_cells:
 //   bound = lo + ldexp(c, -lvl) * width   (multiply, then add)
@@ -95,8 +125,8 @@ __device__ __forceinline__ double mindist2_cell(int lvl, uint32_t code, const Re
   const double xh = __dadd_rn(r.x_lo, __dmul_rn(__dmul_rn((double)(cx + 1), s), r.w));
   const double yl = __dadd_rn(r.y_lo, __dmul_rn(__dmul_rn((double)cy, s), r.h));
   const double yh = __dadd_rn(r.y_lo, __dmul_rn(__dmul_rn((double)(cy + 1), s), r.h));
-  const double dx = fmax(fmax(__dsub_rn(xl, qx), __dsub_rn(qx, xh)), 0.0);
-  const double dy = fmax(fmax(__dsub_rn(yl, qy), __dsub_rn(qy, yh)), 0.0);
+  const double dx = dmax(dmax(__dsub_rn(xl, qx), __dsub_rn(qx, xh)), 0.0);
+  const double dy = dmax(dmax(__dsub_rn(yl, qy), __dsub_rn(qy, yh)), 0.0);
   return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
 }
 

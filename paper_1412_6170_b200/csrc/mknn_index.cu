@@ -41,7 +41,7 @@ __global__ void k_hist_lmax(const double* __restrict__ x, const double* __restri
                             Region r, int l_max, int32_t* __restrict__ cnt) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    atomicAdd(&cnt[encode(x[i], y[i], r, l_max)], 1);
+    atomicAdd(&cnt[encode16(x[i], y[i], r) >> (2 * (16 - l_max))], 1);
   }
 }
 
@@ -128,14 +128,6 @@ __global__ void k_leaf_table(const int32_t* __restrict__ flags, const int32_t* _
   }
 }
 
-// geometry.py:105-129 cell_coord for a given t (shared by two levels)
-__device__ __forceinline__ uint32_t coord_at(double t, int level) {
-  const double n = pow2_pos(level);
-  double c = floor(__dmul_rn(t, n));  // x 2^L is exact
-  c = fmax(c, 0.0);
-  c = fmin(c, n - 1.0);
-  return (uint32_t)c;
-}
 
 // Per point: the leaf (encode at l_deep -> z_map, quadindex.py:196-199;
 // engine.py:206) and the sub-cell key sub_base[leaf] + sub, where sub is the
@@ -148,14 +140,11 @@ __device__ __forceinline__ void point_key(double xi, double yi, const Region& r,
                                           const uint8_t* __restrict__ sub_bits,
                                           const int32_t* __restrict__ sub_base, uint32_t& leaf,
                                           uint32_t& key) {
-  const double tx = (r.w > 0.0) ? __ddiv_rn(__dsub_rn(xi, r.x_lo), r.w) : 0.0;
-  const double ty = (r.h > 0.0) ? __ddiv_rn(__dsub_rn(yi, r.y_lo), r.h) : 0.0;
-  const uint32_t code = spread_bits32(coord_at(tx, l_deep)) | (spread_bits32(coord_at(ty, l_deep)) << 1);
-  leaf = (uint32_t)__ldg(&z_map[code]);
+  const uint32_t f = encode16(xi, yi, r);
+  leaf = (uint32_t)__ldg(&z_map[f >> (2 * (16 - l_deep))]);
   const int sb = __ldg(&sub_bits[leaf]);
   uint32_t sub = 0;
   if (sb) {
-    const uint32_t f = spread_bits32(coord_at(tx, 16)) | (spread_bits32(coord_at(ty, 16)) << 1);
     const int lvl = __ldg(&leaf_level[leaf]);
     sub = (f >> (2 * (16 - lvl) - sb)) & ((1u << sb) - 1u);
   }
@@ -171,8 +160,8 @@ __global__ void k_point_keys(const double* __restrict__ x, const double* __restr
                              uint32_t* __restrict__ key_out, int32_t* __restrict__ cnt,
                              unsigned long long* clamped, int bshift,
                              int32_t* __restrict__ bucket_cnt) {
-  // bucket_cnt != nullptr: count coarse buckets (key >> bshift) through a
-  // block histogram instead of counting every key in global memory
+  // every key is counted in cnt; bucket_cnt != nullptr also counts the coarse
+  // buckets (key >> bshift) of the store partition through a block histogram
   __shared__ int bh[PT_BUCKETS];
   if (bucket_cnt) {
     for (int i = threadIdx.x; i < PT_BUCKETS; i += blockDim.x) bh[i] = 0;
@@ -200,10 +189,8 @@ __global__ void k_point_keys(const double* __restrict__ x, const double* __restr
         point_key(xi[u], yi[u], r, l_deep, z_map, leaf_level, sub_bits, sub_base, leaf, key);
         if (leaf_out) leaf_out[i] = leaf;
         key_out[i] = key;
-        if (bucket_cnt)
-          atomicAdd(&bh[key >> bshift], 1);
-        else
-          atomicAdd(&cnt[key], 1);
+        atomicAdd(&cnt[key], 1);
+        if (bucket_cnt) atomicAdd(&bh[key >> bshift], 1);
       }
     }
   }
@@ -287,65 +274,19 @@ __global__ void __launch_bounds__(PT_THREADS) k_partition(
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < PT_ITEMS; j++)
-    if (t + j * PT_THREADS < tile_n) out[gbase[rc[j].key >> bshift] + rank[j]] = rc[j];
+    if (t + j * PT_THREADS < tile_n) st_rec(&out[gbase[rc[j].key >> bshift] + rank[j]], rc[j]);
 }
 
-// Pass 2: one CTA per bucket: counting sort of the bucket's records by key
-// in shared memory (count, scan, scatter), writing kstart for the bucket's
-// keys and the records into their final slots (an L2-local window).
-constexpr int BS_THREADS = 512;
-
-__global__ void __launch_bounds__(BS_THREADS) k_bucket_sort(
-    const StoreRec* __restrict__ rec, const int32_t* __restrict__ bstart, int bshift, int64_t n_sub,
-    int32_t* __restrict__ kstart, StoreRec* __restrict__ obj) {
-  extern __shared__ int sh[];  // 2^bshift counters
-  __shared__ int wt[BS_THREADS / 32 + 1];
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int b = blockIdx.x;
-  const int bs = bstart[b], be = bstart[b + 1];
-  const int64_t k0 = (int64_t)b << bshift;
-  if (k0 >= n_sub) return;
-  const int kw = (int)min((int64_t)1 << bshift, n_sub - k0);
-  for (int i = t; i < kw; i += BS_THREADS) sh[i] = 0;
-  __syncthreads();
-  for (int i = bs + t; i < be; i += BS_THREADS) atomicAdd(&sh[rec[i].key - k0], 1);
-  __syncthreads();
-  // exclusive scan of sh[0..kw): thread t owns a contiguous run
-  const int per = (kw + BS_THREADS - 1) / BS_THREADS;
-  const int lo = min(t * per, kw), hi = min(lo + per, kw);
-  int sum = 0;
-  for (int i = lo; i < hi; i++) sum += sh[i];
-  int inc = sum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int u = __shfl_up_sync(FULL, inc, o);
-    if (lane >= o) inc += u;
-  }
-  if (lane == 31) wt[w] = inc;
-  __syncthreads();
-  if (w == 0) {
-    const int sv = lane < BS_THREADS / 32 ? wt[lane] : 0;
-    int si = sv;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int u = __shfl_up_sync(FULL, si, o);
-      if (lane >= o) si += u;
-    }
-    if (lane < BS_THREADS / 32) wt[lane] = si - sv;
-  }
-  __syncthreads();
-  int run = bs + inc - sum + wt[w];
-  for (int i = lo; i < hi; i++) {
-    const int c = sh[i];
-    sh[i] = run;
-    kstart[k0 + i] = run;
-    run += c;
-  }
-  if (k0 + kw == n_sub && hi == kw && lo < hi) kstart[n_sub] = run;
-  __syncthreads();
-  for (int i = bs + t; i < be; i += BS_THREADS) {
-    const StoreRec rc = rec[i];
-    obj[atomicAdd(&sh[rc.key - k0], 1)] = rc;
+// Pass 2: final counting-sort scatter, reading the partitioned records in
+// bucket order, so the random 32-byte writes of the moment fall inside an
+// L2-resident window of a few buckets; cnt counts down to zero again.
+__global__ void k_final_scatter(const StoreRec* __restrict__ rec, int64_t n,
+                                const int32_t* __restrict__ kstart, int32_t* __restrict__ cnt,
+                                StoreRec* __restrict__ obj) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const StoreRec rc = ld_rec(&rec[i]);
+    st_rec(&obj[kstart[rc.key] + atomicSub(&cnt[rc.key], 1) - 1], rc);
   }
 }
 
@@ -580,7 +521,7 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
   if (n > 0)
     MKNN_LAUNCH k_point_keys<<<grid_stride_blocks(n), TPB, 0, s>>>(
         x, y, n, r, ix.scalars, ix.z_map, ix.leaf_level, ix.leaf_sub_bits, ix.leaf_sub_base,
-        nullptr, st.key, nullptr, dev_clamped, bshift, st.cursor);
+        nullptr, st.key, st.cnt, dev_clamped, bshift, st.cursor);
   MKNN_CUDA_OK(cudaGetLastError());
   MKNN_LAUNCH k_bucket_scan<<<1, PT_BUCKETS, 0, s>>>(st.cursor, st.bstart, st.cursor);
   if (n > 0) {
@@ -588,22 +529,16 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
         ids, x, y, st.key, n, bshift, st.cursor, st.rec);
     MKNN_CUDA_OK(cudaGetLastError());
   }
-  const size_t bs_smem = sizeof(int32_t) << bshift;
-  if (bs_smem > 48 * 1024) {
-    static size_t configured = 0;
-    if (bs_smem > configured) {
-      MKNN_CUDA_OK(cudaFuncSetAttribute(k_bucket_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)bs_smem));
-      configured = bs_smem;
-    }
-  }
-  MKNN_LAUNCH k_bucket_sort<<<nb, BS_THREADS, bs_smem, s>>>(st.rec, st.bstart, bshift, n_sub,
-                                                           st.kstart, st.obj);
+  int rc = exclusive_scan_i32(st.cnt, st.kstart, n_sub, scratch, s);
+  if (rc) return rc;
+  if (n > 0)
+    MKNN_LAUNCH k_final_scatter<<<grid_stride_blocks(n), TPB, 0, s>>>(st.rec, n, st.kstart, st.cnt,
+                                                                     st.obj);
   MKNN_CUDA_OK(cudaGetLastError());
   MKNN_LAUNCH k_leaf_ranges<<<blocks_for(n_leaves + 1), TPB, 0, s>>>(st.kstart, ix.leaf_sub_base,
                                                                     n_leaves, st.cell_start, st.nch);
   MKNN_CUDA_OK(cudaGetLastError());
-  int rc = exclusive_scan_i32(st.nch, st.chunk_start, n_leaves, scratch, s);
+  rc = exclusive_scan_i32(st.nch, st.chunk_start, n_leaves, scratch, s);
   if (rc) return rc;
   if (n > 0) {
     MKNN_LAUNCH k_chunk_ranges<<<blocks_for(n_leaves), TPB, 0, s>>>(st.cell_start, st.chunk_start,
@@ -616,9 +551,16 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
   return 0;
 }
 
+int issuer_bits(int64_t lo, int64_t hi) {
+  const uint64_t range = (uint64_t)hi - (uint64_t)lo;
+  return range ? 64 - __builtin_clzll(range) : 0;
+}
+
 int queries_index(DevQueries& dq, DevStore& st, const DevIndex& ix, const Region& r,
                   const long long* qi, const double* qx, const double* qy, int64_t nq,
-                  int64_t n_sub, long long* out_qids, void* scratch, cudaStream_t s) {
+                  int64_t n_sub, int plan_bits, int* bits_used, long long* out_qids, void* scratch,
+                  cudaStream_t s) {
+  *bits_used = 0;
   if (nq == 0) return 0;
   MKNN_LAUNCH k_point_keys<<<grid_stride_blocks(nq), TPB, 0, s>>>(
       qx, qy, nq, r, ix.scalars, ix.z_map, ix.leaf_level, ix.leaf_sub_bits, ix.leaf_sub_base,
@@ -630,14 +572,21 @@ int queries_index(DevQueries& dq, DevStore& st, const DevIndex& ix, const Region
                                                                 dq.order);
   MKNN_CUDA_OK(cudaGetLastError());
 
-  // stable issuer order for emission (engine.py:713 / oracle.py:56)
+  // stable issuer order for emission (engine.py:713 / oracle.py:56): LSD
+  // radix sort of (issuer - min) over plan_bits bits.  plan_bits < 0: read
+  // the range first (one host sync); otherwise the caller planned from the
+  // previous tick and checks dq.minmax after the tick (mknn_api.cu retries
+  // the tick if the range needed more bits).
   rc = minmax_i64((const int64_t*)qi, nq, dq.minmax, s);
   if (rc) return rc;
-  int64_t mm[2];
-  MKNN_CUDA_OK(cudaMemcpyAsync(mm, dq.minmax, sizeof(mm), cudaMemcpyDeviceToHost, s));
-  MKNN_CUDA_OK(cudaStreamSynchronize(s));
-  const uint64_t range = (uint64_t)mm[1] - (uint64_t)mm[0];
-  const int bits = range ? 64 - __builtin_clzll(range) : 0;
+  int bits = plan_bits;
+  if (bits < 0) {
+    int64_t mm[2];
+    MKNN_CUDA_OK(cudaMemcpyAsync(mm, dq.minmax, sizeof(mm), cudaMemcpyDeviceToHost, s));
+    MKNN_CUDA_OK(cudaStreamSynchronize(s));
+    bits = issuer_bits(mm[0], mm[1]);
+  }
+  *bits_used = bits;
   MKNN_LAUNCH k_issuer_keys<<<blocks_for(nq), TPB, 0, s>>>(qi, nq, dq.minmax, dq.keys, dq.vals);
   MKNN_CUDA_OK(cudaGetLastError());
   bool alt = false;

@@ -94,6 +94,26 @@ struct __align__(32) StoreRec {  // one object of the leaf-sorted store
   uint32_t key, pad;
 };
 
+// 256-bit global accesses (sm_100: LDG/STG.E.ENL2.256): one request per record
+__device__ __forceinline__ StoreRec ld_rec(const StoreRec* p) {
+  unsigned long long a, b, c, d;
+  asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+  StoreRec r;
+  r.x = __longlong_as_double((long long)a);
+  r.y = __longlong_as_double((long long)b);
+  r.id = (long long)c;
+  r.key = (uint32_t)d;
+  r.pad = (uint32_t)(d >> 32);
+  return r;
+}
+__device__ __forceinline__ void st_rec(StoreRec* p, const StoreRec& r) {
+  asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p),
+               "l"((unsigned long long)__double_as_longlong(r.x)),
+               "l"((unsigned long long)__double_as_longlong(r.y)), "l"((unsigned long long)r.id),
+               "l"((unsigned long long)r.key | ((unsigned long long)r.pad << 32))
+               : "memory");
+}
+
 struct DevStore {
   StoreRec* obj = nullptr;        // leaf-sorted objects
   StoreRec* rec = nullptr;        // staging of the bucket partition pass
@@ -138,9 +158,14 @@ struct DevQueries {
 };
 
 // uses st.sub_cnt / st.sub_start as its counting-sort tables
+// plan_bits: issuer-id bits to sort on (< 0: measure them first, one host
+// sync); *bits_used receives the bits actually sorted on
 int queries_index(DevQueries& dq, DevStore& st, const DevIndex& ix, const Region& r,
                   const long long* qi, const double* qx, const double* qy, int64_t nq,
-                  int64_t n_sub, long long* out_qids, void* scratch, cudaStream_t s);
+                  int64_t n_sub, int plan_bits, int* bits_used, long long* out_qids, void* scratch,
+                  cudaStream_t s);
+// bits of the issuer-id range [lo, hi]
+int issuer_bits(int64_t lo, int64_t hi);
 
 // ------------------------------------------------------------- search
 struct QueryStats {

@@ -72,55 +72,90 @@ __device__ __forceinline__ T block_excl_scan(T v, T* sh_warp, T& total) {
   return r;
 }
 
-__global__ void k_tile_sums(const int32_t* __restrict__ in, int64_t n, long long* sums) {
-  __shared__ long long sh[33];
-  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
-  long long acc = 0;
-#pragma unroll
-  for (int i = 0; i < SCAN_ITEMS; i++) {
-    int64_t idx = base + (int64_t)i * SCAN_THREADS + threadIdx.x;
-    if (idx < n) acc += in[idx];
-  }
-  long long tot;
-  block_excl_scan<long long>(acc, sh, tot);
-  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
-}
+// Single-pass scan with decoupled look-back: each tile publishes its
+// aggregate, then its inclusive prefix once the predecessor prefixes are
+// known; tile ids come from an atomic counter so every tile's predecessors
+// are already running (forward progress).  Status word: value << 2 | flag
+// (flag 1 = aggregate only, 2 = inclusive prefix; 0 = not yet published).
+constexpr unsigned long long ST_AGG = 1, ST_PREFIX = 2;
 
-__global__ void k_scan_sums(long long* sums, int64_t nb) {
-  __shared__ long long sh[33];
-  long long carry = 0;
-  for (int64_t base = 0; base < nb; base += blockDim.x) {
-    int64_t i = base + threadIdx.x;
-    long long v = i < nb ? sums[i] : 0;
-    long long tot;
-    long long ex = block_excl_scan<long long>(v, sh, tot);
-    if (i < nb) sums[i] = ex + carry;
-    carry += tot;
-  }
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 template <typename TO>
-__global__ void k_tile_apply(const int32_t* __restrict__ in, TO* __restrict__ out, int64_t n,
-                             const long long* __restrict__ sums) {
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_lookback(
+    const int32_t* __restrict__ in, TO* __restrict__ out, int64_t n, int64_t n_tiles,
+    unsigned long long* status, unsigned int* tile_ctr) {
   __shared__ long long sh[33];
-  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+  __shared__ long long tile_excl;
+  __shared__ int tile_sh;
+  if (threadIdx.x == 0) tile_sh = (int)atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const int64_t tile = tile_sh;
+  const int64_t base = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
   int32_t v[SCAN_ITEMS];
+  if (base + SCAN_ITEMS <= n && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; i += 4) {
+      const int4 q = *reinterpret_cast<const int4*>(&in[base + i]);
+      v[i] = q.x;
+      v[i + 1] = q.y;
+      v[i + 2] = q.z;
+      v[i + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; i++) v[i] = base + i < n ? in[base + i] : 0;
+  }
   long long acc = 0;
 #pragma unroll
-  for (int i = 0; i < SCAN_ITEMS; i++) {
-    int64_t idx = base + i;
-    v[i] = idx < n ? in[idx] : 0;
-    acc += v[i];
-  }
+  for (int i = 0; i < SCAN_ITEMS; i++) acc += v[i];
   long long tot;
-  long long ex = block_excl_scan<long long>(acc, sh, tot) + sums[blockIdx.x];
+  long long ex = block_excl_scan<long long>(acc, sh, tot);
+  // look-back (warp 0): 32 predecessors per round
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    if (lane == 0)
+      st_status(&status[tile], ((unsigned long long)tot << 2) | (tile == 0 ? ST_PREFIX : ST_AGG));
+    long long prefix = 0;
+    if (tile > 0) {
+      int64_t j = tile - 1;
+      for (;;) {
+        const int64_t p = j - lane;
+        unsigned long long st = ST_PREFIX;  // beyond tile 0: neutral
+        if (p >= 0) {
+          do {
+            st = ld_status(&status[p]);
+          } while ((st & 3ull) == 0);
+        }
+        const bool is_prefix = p < 0 || (st & 3ull) == ST_PREFIX;
+        const unsigned pm = __ballot_sync(FULL, is_prefix);
+        const int stop = __ffs(pm) - 1;  // nearest predecessor with a full prefix
+        long long val = (p >= 0 && (pm == 0 || lane <= stop)) ? (long long)(st >> 2) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(FULL, val, o);
+        prefix += val;
+        if (pm) break;
+        j -= 32;
+      }
+      if (lane == 0) st_status(&status[tile], ((unsigned long long)(prefix + tot) << 2) | ST_PREFIX);
+    }
+    if (lane == 0) tile_excl = prefix;
+  }
+  __syncthreads();
+  ex += tile_excl;
 #pragma unroll
   for (int i = 0; i < SCAN_ITEMS; i++) {
-    int64_t idx = base + i;
-    if (idx < n) out[idx] = (TO)ex;
+    if (base + i < n) out[base + i] = (TO)ex;
     ex += v[i];
   }
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) out[n] = (TO)ex;
+  if (tile == n_tiles - 1 && threadIdx.x == blockDim.x - 1) out[n] = (TO)ex;
 }
 
 template <typename TO>
@@ -134,10 +169,10 @@ int exclusive_scan_impl(const int32_t* in, TO* out, int64_t n, void* scratch, cu
     return 0;
   }
   const int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
-  long long* sums = (long long*)scratch;
-  MKNN_LAUNCH k_tile_sums<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, n, sums);
-  MKNN_LAUNCH k_scan_sums<<<1, 1024, 0, s>>>(sums, nb);
-  MKNN_LAUNCH k_tile_apply<TO><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, out, n, sums);
+  unsigned long long* status = (unsigned long long*)scratch;
+  unsigned int* ctr = (unsigned int*)(status + nb);
+  MKNN_CUDA_OK(cudaMemsetAsync(scratch, 0, sizeof(unsigned long long) * (nb + 1), s));
+  MKNN_LAUNCH k_scan_lookback<TO><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, out, n, nb, status, ctr);
   MKNN_CUDA_OK(cudaGetLastError());
   return 0;
 }
@@ -145,7 +180,7 @@ int exclusive_scan_impl(const int32_t* in, TO* out, int64_t n, void* scratch, cu
 }  // namespace
 
 size_t scan_scratch_bytes(int64_t n) {
-  return sizeof(long long) * (size_t)((n + SCAN_TILE - 1) / SCAN_TILE + 1);
+  return sizeof(long long) * (size_t)((n + SCAN_TILE - 1) / SCAN_TILE + 2);
 }
 
 int exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* scratch,

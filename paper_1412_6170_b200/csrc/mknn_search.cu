@@ -46,13 +46,6 @@ namespace mknn {
 
 namespace {
 
-__device__ __forceinline__ double2 obj_xy(const StoreRec* __restrict__ obj, int i) {
-  return __ldg(reinterpret_cast<const double2*>(&obj[i]));
-}
-__device__ __forceinline__ long long obj_id(const StoreRec* __restrict__ obj, int i) {
-  return __ldg(&obj[i].id);
-}
-
 template <int KPL>
 struct List {
   double d[KPL];
@@ -314,36 +307,32 @@ __device__ __forceinline__ void admit(List<KPL>& L, double cd0, long long ci0, u
 }
 
 // engine.py:279-324 _merge_pack for one row restricted to one chunk of a
-// leaf: every object of [beg, end) (<= 32) except the issuer (by id,
-// engine.py:298-300) competes for the list; admission is (d2, id) < k-th.
+// leaf (one record per lane, already loaded): every object except the issuer
+// (by id, engine.py:298-300) competes for the list; admission is
+// (d2, id) < k-th.  Returns whether the list changed.
 template <int KPL>
-__device__ __forceinline__ bool scan_chunk(List<KPL>& L, double kd, long long ki, int beg, int end,
-                                           double qx, double qy, long long me,
-                                           const StoreRec* __restrict__ obj, int lane,
-                                           unsigned long long* prof) {
-  const int idx = beg + lane;
-  bool pass = false;
-  double d2 = DINF;
-  long long id = IDMAX;
-  if (idx < end) {
-    const double2 p = obj_xy(obj, idx);
-    d2 = pair_d2(qx, qy, p.x, p.y);
-    if (d2 <= kd) {
-      id = obj_id(obj, idx);
-      pass = (id != me) && key_less(d2, id, kd, ki);
-    }
-  }
+__device__ __forceinline__ bool scan_rec(List<KPL>& L, double kd, long long ki, bool valid,
+                                         const StoreRec& r, double qx, double qy, long long me,
+                                         int lane, unsigned long long* prof) {
+  const double d2 = valid ? pair_d2(qx, qy, r.x, r.y) : DINF;
+  const bool pass = valid && d2 <= kd && r.id != me && key_less(d2, r.id, kd, ki);
   const unsigned m = __ballot_sync(FULL, pass);
-  if (m) admit<KPL>(L, pass ? d2 : DINF, pass ? id : IDMAX, m, lane, prof);
+  if (m) admit<KPL>(L, pass ? d2 : DINF, pass ? r.id : IDMAX, m, lane, prof);
   return m != 0;
+}
+
+__device__ __forceinline__ StoreRec load_rec(const StoreRec* __restrict__ obj, int i, bool valid) {
+  StoreRec r;
+  if (valid) r = ld_rec(&obj[i]);
+  return r;
 }
 
 // min-dist2 from the query to a chunk's point bounding box: a lower bound of
 // pair_d2 for every object of the chunk (each step is a correctly rounded,
 // monotone operation of the same inputs pair_d2 rounds; geometry.py:189-193)
 __device__ __forceinline__ double mindist2_box(const ChunkBox& b, double qx, double qy) {
-  const double dx = fmax(fmax(__dsub_rn(b.x_lo, qx), __dsub_rn(qx, b.x_hi)), 0.0);
-  const double dy = fmax(fmax(__dsub_rn(b.y_lo, qy), __dsub_rn(qy, b.y_hi)), 0.0);
+  const double dx = dmax(dmax(__dsub_rn(b.x_lo, qx), __dsub_rn(qx, b.x_hi)), 0.0);
+  const double dy = dmax(dmax(__dsub_rn(b.y_lo, qy), __dsub_rn(qy, b.y_hi)), 0.0);
   return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
 }
 
@@ -377,9 +366,10 @@ __device__ __forceinline__ void visit_leaf(List<KPL>& L, int k, int leaf, double
       const int src = (int)(__reduce_min_sync(FULL, key) & 31u);
       if (lane == src) live = false;
       const int cb = ob + (g - c0 + src) * CHUNK;
+      const bool v = cb + lane < min(cb + CHUNK, oe);
+      const StoreRec r = load_rec(a.obj, cb + lane, v);
       prof_add(a.prof, own ? PROF_OWN_CHUNKS_SCANNED : PROF_EXP_CHUNKS_SCANNED, 1, lane);
-      if (scan_chunk<KPL>(L, kd, ki, cb, min(cb + CHUNK, oe), qx, qy, me, a.obj, lane, a.prof))
-        list_kth<KPL>(L, k, kd, ki);
+      if (scan_rec<KPL>(L, kd, ki, v, r, qx, qy, me, lane, a.prof)) list_kth<KPL>(L, k, kd, ki);
     }
   }
 }
@@ -715,7 +705,14 @@ int search_launch(const SearchArgs& a, cudaStream_t s) {
   if (a.nq == 0) return 0;
   // k <= 32: 16 queries per warp, 4 warps per CTA, <= 80 registers: the
   // occupancy/latency optimum measured on B200
-  if (a.k <= 32) return launch_batched<1, 16, 4, 6>(a, s);
+  if (a.k <= 32) {
+    static const char* v = getenv("MKNN_B");  // profiling only: batch / warps variants
+    const int b = v ? atoi(v) : 0;
+    if (b == 1) return launch_batched<1, 32, 2, 12>(a, s);
+    if (b == 2) return launch_batched<1, 32, 4, 6>(a, s);
+    if (b == 3) return launch_batched<1, 16, 4, 8>(a, s);
+    return launch_batched<1, 16, 4, 6>(a, s);
+  }
   if (a.k <= 64) return launch_batched<2, 16, 4>(a, s);
   if (a.k <= 128) return launch_batched<4, 8, 4>(a, s);
   if (a.k <= 256) return launch_batched<8, 4, 4>(a, s);

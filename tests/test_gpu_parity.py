@@ -211,3 +211,62 @@ def test_large_vs_oracle_engine_port(dist, n, nq, k, seed):
     assert m.pruned_leaves == want.metrics["pruned_leaves"]
     assert m.active_left == want.metrics["active_left"]
     assert m.active_right == want.metrics["active_right"]
+
+
+def test_issuer_range_growth_between_ticks():
+    """The issuer-order sort is planned from the previous tick's issuer-id
+    range; a tick whose range needs more bits must still come out in issuer
+    order (the engine re-runs it with the measured range)."""
+    rng = np.random.default_rng(21)
+    n = 3000
+    x = rng.uniform(0, 500, n)
+    y = rng.uniform(0, 500, n)
+    ids = np.arange(n, dtype=np.int64)
+    region = Rect.square(500.0)
+    with Engine(EngineConfig(k=9, region=region, th_quad=32)) as eng:
+        for t, span in enumerate([40, 40, 1 << 40, 3, 1 << 62]):
+            nq = 200
+            sel = rng.choice(n, nq, replace=False)
+            qx, qy = x[sel], y[sel]
+            qi = (rng.integers(0, span, nq) if span > 1 else np.zeros(nq, np.int64)).astype(np.int64)
+            qi[: nq // 2] = ids[sel[: nq // 2]]
+            res = eng.process_tick(ids, x, y, qi, qx, qy)
+            assert_same(res, orc.brute_force_knn(ids, x, y, qi, qx, qy, 9))
+            assert eng.last_metrics.tick == t
+
+
+@pytest.mark.parametrize("lo,width", [(0.0, 22500.0), (-7.3, 1000.1), (1e6 + 0.1, 3.0)])
+def test_cell_borders_match_reference_encoding(lo, width):
+    """Objects exactly on (and one ulp either side of) quadrant borders at
+    every level: the device's reciprocal fast path must floor exactly like
+    the reference's IEEE division (geometry.py:105-129), so the index and the
+    per-leaf cell ranges equal the oracle's build_index / index_objects."""
+    rng = np.random.default_rng(int(width))
+    region = Rect(lo, lo, lo + width, lo + width)
+    pts = []
+    for lvl in (1, 3, 5, 8, 10, 13, 16):
+        c = rng.integers(0, 2 ** lvl, 300)
+        b = lo + np.ldexp(c.astype(np.float64), -lvl) * width
+        for v in (b, np.nextafter(b, -np.inf), np.nextafter(b, np.inf)):
+            pts.append(v)
+    xs = np.concatenate(pts)
+    ys = rng.permutation(xs)
+    xs = np.concatenate([xs, [lo, lo + width, lo - 1.0, lo + width + 1.0]])
+    ys = np.concatenate([ys, [lo + width, lo, lo + 0.5 * width, lo - 3.0]])
+    n = len(xs)
+    ids = np.arange(n, dtype=np.int64)
+    th, l_max = 8, 10
+    want_ix = orc.build_index(xs, ys, region, th, l_max)
+    want_st = orc.index_objects(ids, xs, ys, region, want_ix)
+    orc.free_index(want_ix)
+    sel = rng.choice(n, 400, replace=False)
+    with Engine(EngineConfig(k=6, region=region, th_quad=th, l_max=l_max)) as eng:
+        res = eng.process_tick(ids, xs, ys, ids[sel], xs[sel], ys[sel])
+        ix = eng.index
+        for key in ("leaf_level", "leaf_code", "leaf_key", "leaf_span", "build_counts"):
+            np.testing.assert_array_equal(getattr(ix, key), want_ix[key], err_msg=key)
+        cs, ce = eng.cell_ranges()
+        np.testing.assert_array_equal(cs, want_st["cell_start"])
+        np.testing.assert_array_equal(ce, want_st["cell_end"])
+        assert eng.last_metrics.clamped_objects == want_st["clamped"]
+    assert_same(res, orc.brute_force_knn(ids, xs, ys, ids[sel], xs[sel], ys[sel], 6))
