@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmknn_b200.so")
+# MKNN_LIB overrides the library path (profiling builds of variants only)
+LIB_PATH = os.environ.get("MKNN_LIB") or os.path.join(_HERE, "libmknn_b200.so")
 
 _i64p = ctypes.POINTER(ctypes.c_int64)
 _i32p = ctypes.POINTER(ctypes.c_int32)
