@@ -374,6 +374,169 @@ __device__ __forceinline__ void visit_leaf(List<KPL>& L, int k, int leaf, double
   }
 }
 
+// ---- multi-slot lists (k > 32): buffered admission ----------------------
+// With N = 32*KPL slots, admitting a chunk at a time would re-merge N keys
+// per chunk.  Candidates that beat the (possibly stale) k-th key are instead
+// appended to a per-warp shared-memory buffer (ballot compaction) and merged
+// N - 32 at a time: one sort of the buffer and one merge into the list, both
+// on 64-bit keys (akey64, source index in the low bits) with the exact values
+// gathered from shared memory afterwards; exact (d2, id) networks only when
+// two neighbours share a truncated key.  A stale k-th key only lets extra
+// candidates into the buffer: the merge keeps the N smallest, so the list
+// is exact.
+template <int KPL, typename KT>
+__device__ __forceinline__ void step_key(KT (&kk)[KPL], int lane, int size, int j) {
+  if (j >= 32) {
+    const int js = j >> 5;
+#pragma unroll
+    for (int s = 0; s < KPL; s++) {
+      if ((s & js) == 0) {
+        const int t = s | js;
+        const bool asc = ((s << 5) & size) == 0;
+        const KT lo = min(kk[s], kk[t]), hi = max(kk[s], kk[t]);
+        kk[s] = asc ? lo : hi;
+        kk[t] = asc ? hi : lo;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < KPL; s++) {
+      const KT p = __shfl_xor_sync(FULL, kk[s], j);
+      const int e = (s << 5) | lane;
+      const bool take_min = ((lane & j) == 0) == ((e & size) == 0);
+      kk[s] = take_min ? min(kk[s], p) : max(kk[s], p);
+    }
+  }
+}
+
+// 64-bit sort key of d2 >= 0: the double's bits (monotone) with the low
+// `bits` bits replaced by a source index; only d2 values within 2^-44
+// relative of each other (or exact ties) share a truncated key
+constexpr unsigned long long AKEY64_INF = 0x7FF0000000000000ull;
+
+__device__ __forceinline__ unsigned long long akey64(double d2, int bits, unsigned src) {
+  return ((unsigned long long)__double_as_longlong(d2) & ~((1ull << bits) - 1ull)) | src;
+}
+
+// neighbours (element e, e + 1) of a KPL-slot key sequence with equal
+// truncated keys (other than sentinels)?
+template <int KPL>
+__device__ __forceinline__ bool akey64_ties(const unsigned long long (&kk)[KPL], int bits, int lane) {
+  bool tie = false;
+#pragma unroll
+  for (int s = 0; s < KPL; s++) {
+    const unsigned long long dn = __shfl_down_sync(FULL, kk[s], 1);
+    const unsigned long long nx =
+        (s + 1 < KPL) ? __shfl_sync(FULL, kk[s + 1 < KPL ? s + 1 : s], 0) : ~0ull;
+    const unsigned long long nk = lane < 31 ? dn : nx;
+    tie |= ((kk[s] ^ nk) >> bits) == 0 && (kk[s] >> bits) < (AKEY64_INF >> bits) &&
+           !(s + 1 == KPL && lane == 31);
+  }
+  return __any_sync(FULL, tie);
+}
+
+// L <- the N smallest of L u buffer[0, nbuf); L ascending.  rowd/rowi: the
+// list's shared-memory home (overwritten), bufd/bufi: the buffer.
+template <int KPL>
+__device__ __noinline__ void merge_buffer(List<KPL>& L, const double* bufd, const long long* bufi,
+                                          int nbuf, double* rowd, long long* rowi, int lane) {
+  constexpr int N = 32 * KPL;
+  constexpr int SB = KPL <= 2 ? 7 : (KPL <= 4 ? 8 : (KPL <= 8 ? 9 : 10));  // bits for 2N sources
+  unsigned long long kb[KPL], m[KPL];
+#pragma unroll
+  for (int s = 0; s < KPL; s++) {
+    const int e = (s << 5) | lane;
+    kb[s] = e < nbuf ? akey64(bufd[e], SB, (unsigned)(N + e)) : (~0ull << SB) | (unsigned)(N + e);
+    rowd[e] = L.d[s];
+    rowi[e] = L.id[s];
+  }
+#pragma unroll
+  for (int size = 2; size <= N; size <<= 1) {
+#pragma unroll
+    for (int j = size >> 1; j > 0; j >>= 1) step_key<KPL>(kb, lane, size, j);
+  }
+  // min(A_e, B_{N-1-e}): the N smallest as a bitonic sequence
+#pragma unroll
+  for (int s = 0; s < KPL; s++) {
+    const unsigned long long kl = akey64(L.d[s], SB, (unsigned)((s << 5) | lane));
+    m[s] = min(kl, __shfl_sync(FULL, kb[KPL - 1 - s], 31 - lane));
+  }
+#pragma unroll
+  for (int j = N >> 1; j > 0; j >>= 1) step_key<KPL>(m, lane, N, j);
+  __syncwarp();
+  if (akey64_ties<KPL>(m, SB, lane)) {  // exact (d2, id) networks
+    double cd[KPL];
+    long long ci[KPL];
+#pragma unroll
+    for (int s = 0; s < KPL; s++) {
+      const int e = (s << 5) | lane;
+      cd[s] = e < nbuf ? bufd[e] : DINF;
+      ci[s] = e < nbuf ? bufi[e] : IDMAX;
+    }
+    bitonic_sort<KPL>(cd, ci, lane);
+    bitonic_merge_into<KPL>(L, cd, ci, lane);
+    __syncwarp();
+    return;
+  }
+#pragma unroll
+  for (int s = 0; s < KPL; s++) {
+    const int src = (int)(m[s] & ((1ull << SB) - 1ull));
+    const bool from_list = src < N, pad = src - N >= nbuf;  // pad: an unused buffer slot
+    L.d[s] = from_list ? rowd[src] : (pad ? DINF : bufd[src - N]);
+    L.id[s] = from_list ? rowi[src] : (pad ? IDMAX : bufi[src - N]);
+  }
+  __syncwarp();
+}
+
+template <int KPL>
+__device__ __forceinline__ void visit_leaf_buf(List<KPL>& L, int k, int leaf, double qx, double qy,
+                                               long long me, const SearchArgs& a, int lane,
+                                               double* bufd, long long* bufi, double* rowd,
+                                               long long* rowi) {
+  constexpr int N = 32 * KPL;
+  const int ob = __ldg(&a.cell_start[leaf]), oe = __ldg(&a.cell_start[leaf + 1]);
+  const int c0 = __ldg(&a.chunk_start[leaf]), c1 = __ldg(&a.chunk_start[leaf + 1]);
+  const unsigned lt = (1u << lane) - 1u;
+  double kd;
+  long long ki;
+  list_kth<KPL>(L, k, kd, ki);
+  int nbuf = 0;
+  for (int g = c0; g < c1; g += 32) {
+    bool live = g + lane < c1;
+    double md = DINF;
+    if (live) md = mindist2_box(a.box[g + lane], qx, qy);
+    for (;;) {
+      const bool cand = live && md <= kd;
+      if (!__any_sync(FULL, cand)) break;
+      const unsigned key =
+          cand ? ((__float_as_uint(__double2float_rd(md)) & ~31u) | (unsigned)lane) : 0xffffffffu;
+      const int src = (int)(__reduce_min_sync(FULL, key) & 31u);
+      if (lane == src) live = false;
+      const int cb = ob + (g - c0 + src) * CHUNK;
+      const bool v = cb + lane < min(cb + CHUNK, oe);
+      const StoreRec r = load_rec(a.obj, cb + lane, v);
+      const double d2 = v ? pair_d2(qx, qy, r.x, r.y) : DINF;
+      const bool pass = v && d2 <= kd && r.id != me && key_less(d2, r.id, kd, ki);
+      const unsigned m = __ballot_sync(FULL, pass);
+      if (m) {
+        if (pass) {
+          const int pos = nbuf + __popc(m & lt);
+          bufd[pos] = d2;
+          bufi[pos] = r.id;
+        }
+        nbuf += __popc(m);
+        __syncwarp();
+        if (nbuf > N - 32) {
+          merge_buffer<KPL>(L, bufd, bufi, nbuf, rowd, rowi, lane);
+          nbuf = 0;
+          list_kth<KPL>(L, k, kd, ki);
+        }
+      }
+    }
+  }
+  if (nbuf) merge_buffer<KPL>(L, bufd, bufi, nbuf, rowd, rowi, lane);
+}
+
 // engine.py:421-431 coarsest_levels: the coarsest quadrant aligned with the
 // cursor (first code for right walks, last code for left walks)
 __device__ __forceinline__ int coarsest_level(long long p, int dir, int l_deep) {
@@ -489,6 +652,10 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double* sd = reinterpret_cast<double*>(smem_raw) + (size_t)w * B * N;
   long long* si = reinterpret_cast<long long*>(smem_raw) + (size_t)WARPS * B * N + (size_t)w * B * N;
+  // k > 32: per-warp admission buffer after the lists
+  double* bufd = reinterpret_cast<double*>(smem_raw) + (size_t)2 * WARPS * B * N + (size_t)w * N;
+  long long* bufi = reinterpret_cast<long long*>(smem_raw) + (size_t)2 * WARPS * B * N +
+                    (size_t)WARPS * N + (size_t)w * N;
   const int64_t t0 = ((int64_t)blockIdx.x * WARPS + w) * B;
   if (t0 >= a.nq) return;
   const int nb = (int)((a.nq - t0) < B ? (a.nq - t0) : B);
@@ -527,7 +694,10 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
       L.d[s] = DINF;
       L.id[s] = IDMAX;
     }
-    visit_leaf<KPL>(L, k, (int)jown, jx, jy, jme, a, lane, true);
+    if constexpr (KPL == 1)
+      visit_leaf<KPL>(L, k, (int)jown, jx, jy, jme, a, lane, true);
+    else
+      visit_leaf_buf<KPL>(L, k, (int)jown, jx, jy, jme, a, lane, bufd, bufi, sd + j * N, si + j * N);
     double kd;
     long long ki;
     list_kth<KPL>(L, k, kd, ki);
@@ -569,7 +739,10 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
       const long long jme = __shfl_sync(FULL, me, j);
       List<KPL> L;
       list_load<KPL>(L, sd + j * N, si + j * N, lane);
-      visit_leaf<KPL>(L, k, jl, jx, jy, jme, a, lane, false);
+      if constexpr (KPL == 1)
+        visit_leaf<KPL>(L, k, jl, jx, jy, jme, a, lane, false);
+      else
+        visit_leaf_buf<KPL>(L, k, jl, jx, jy, jme, a, lane, bufd, bufi, sd + j * N, si + j * N);
       list_store<KPL>(L, sd + j * N, si + j * N, lane);
       double kd;
       long long ki;
@@ -687,7 +860,7 @@ __global__ void k_rows_compact(const int32_t* __restrict__ len, const long long*
 template <int KPL, int B, int WARPS, int MINB = 1>
 int launch_batched(const SearchArgs& a, cudaStream_t s) {
   constexpr int N = 32 * KPL;
-  const size_t smem = (size_t)WARPS * B * N * (sizeof(double) + sizeof(long long));
+  const size_t smem = (size_t)WARPS * (B + (KPL > 1 ? 1 : 0)) * N * (sizeof(double) + sizeof(long long));
   static bool configured = false;
   if (!configured) {
     MKNN_CUDA_OK(cudaFuncSetAttribute(k_search<KPL, B, WARPS, MINB>,
