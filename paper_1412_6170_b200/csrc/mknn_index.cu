@@ -345,7 +345,8 @@ __global__ void k_chunk_boxes(const StoreRec* __restrict__ obj, const int2* __re
 }
 
 // rebuild: 4^s sub-cells per leaf with s the smallest level count that
-// leaves <= 4 build-time objects per sub-cell (s <= 5)
+// leaves <= 4 build-time objects per sub-cell (s <= 5, and the table of all
+// leaves' sub-cells capped at 2^24 counters so its atomics stay in L2)
 __global__ void k_leaf_subs(const int32_t* __restrict__ build_counts,
                             const int32_t* __restrict__ scalars, int64_t ncap,
                             uint8_t* __restrict__ sub_bits, int32_t* __restrict__ sub_size) {
@@ -355,9 +356,13 @@ __global__ void k_leaf_subs(const int32_t* __restrict__ build_counts,
     sub_size[l] = 0;
     return;
   }
+  // cap: the whole sub-cell table stays <= 2^24 counters (L2-resident)
+  const int64_t nl = scalars[1];
+  int cap = 0;
+  while (cap < 5 && (nl << (2 * (cap + 1))) <= (int64_t(1) << 24)) cap++;
   const int c = build_counts[l];
   int sl = 0;
-  while (sl < 5 && c > (4 << (2 * sl))) sl++;
+  while (sl < cap && c > (4 << (2 * sl))) sl++;
   sub_bits[l] = (uint8_t)(2 * sl);
   sub_size[l] = 1 << (2 * sl);
 }
