@@ -2,22 +2,27 @@
 """Benchmark of the per-tick repeated k-NN join (BASELINE.json metric).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
-                    [--workload cfg3|cfg3u|cfg2|cfg4|k1|k8|k32|k128]
+                    [--workload cfg3|cfg3u|cfg2|cfg2s|cfg4|cfg4s|k1|k8|k32|k128]
 
-A step is one tick: a full position snapshot of n objects plus a batch of
-queries -> every query's k nearest (id, distance) lists, CSR in issuer order.
+A step is one tick -> every query's k nearest (id, distance) lists, CSR in
+issuer order.  Snapshot workloads (cfg3, cfg3u, k*, cfg2s, cfg4s) hand the
+engine the full position snapshot every tick; delta workloads (cfg2, cfg4:
+BASELINE.json's "10% position updates per tick") hand it the tick's U
+position updates over the device-resident snapshot (carry-forward semantics
+of datasets.py:136-148).
 Default workload (the metric is quoted "at 10M objects"): BASELINE.json
 configs[2], Gaussian-clustered n=10M (16 hotspots, sigma 500), 1M queries,
 k=32; synthetic data from the reference generator's placement draws
 (paper_1412_6170_b200/synth.py).
 
 * value: queries/s of the whole job with inputs resident in HBM
-  (Engine.tick_device: full snapshot + queries already on the device), timed
-  with CUDA events per step on the launching stream, L2 flushed between
-  steps outside the timed events, max over ranks.
+  (Engine.tick_device, or Engine.update + Engine.query_device for delta
+  workloads), timed with CUDA events per step on the launching stream, L2
+  flushed between steps outside the timed events, max over ranks.
 * e2e: the same metric through the reference-facing API (Engine.process_tick
-  -> C-ABI mknn_tick) with pinned HOST buffers: the H2D of the snapshot and
-  the queries and the D2H of the result CSR are inside every timed step.
+  -> C-ABI mknn_tick, or Engine.update + Engine.query) with pinned HOST
+  buffers: the H2D of the snapshot or updates and the queries and the D2H of
+  the result CSR are inside every timed step.
 * roofline: the dominant kernel (k_search); algorithmic bytes per launch =
   24*T + 24*Q + 16*Q*k (T = records the reference's distance tasks stream,
   counted on device in one extra untimed instrumented step), divided by the
@@ -25,8 +30,9 @@ k=32; synthetic data from the reference generator's placement draws
 * cpu_baseline: the C port of the reference engine (oracle/, OpenMP, all host
   threads) on a bounded sample, scaled to one tick.
 * --gpus N>1 (torchrun): weak scaling, each rank answers 1M queries of its
-  own against the replicated snapshot, whose 1/N slices are all-gathered
-  over NCCL every step (sharded.py).
+  own against the replicated snapshot; the snapshot (or the tick's updates)
+  arrive as 1/N slices per rank and are all-gathered over NCCL every step
+  (sharded.py).
 """
 
 from __future__ import annotations
@@ -51,10 +57,16 @@ WORKLOADS = {
                  dist="gaussian", n=10_000_000, nq=1_000_000, k=32, seed=3, baseline_idx=2),
     "cfg3u": dict(desc="uniform 10M objects, 1M queries, k=32", dist="uniform", n=10_000_000,
                   nq=1_000_000, k=32, seed=3, baseline_idx=2),
-    "cfg2": dict(desc="uniform 1M objects, 100K queries, k=32", dist="uniform", n=1_000_000,
-                 nq=100_000, k=32, seed=0, baseline_idx=1),
-    "cfg4": dict(desc="uniform 100M objects, 10M queries, k=16", dist="uniform", n=100_000_000,
-                 nq=10_000_000, k=16, seed=4, baseline_idx=3),
+    "cfg2": dict(desc="uniform 1M objects, 100K queries, k=32, 10% position updates per tick",
+                 dist="uniform", n=1_000_000, nq=100_000, k=32, seed=0, baseline_idx=1,
+                 updates=0.10),
+    "cfg2s": dict(desc="uniform 1M objects, 100K queries, k=32, full snapshot per tick",
+                  dist="uniform", n=1_000_000, nq=100_000, k=32, seed=0, baseline_idx=1),
+    "cfg4": dict(desc="uniform 100M objects, 10M queries, k=16, 10% position updates per tick",
+                 dist="uniform", n=100_000_000, nq=10_000_000, k=16, seed=4, baseline_idx=3,
+                 updates=0.10),
+    "cfg4s": dict(desc="uniform 100M objects, 10M queries, k=16, full snapshot per tick",
+                  dist="uniform", n=100_000_000, nq=10_000_000, k=16, seed=4, baseline_idx=3),
 }
 for _k in (1, 8, 32, 128):
     WORKLOADS[f"k{_k}"] = dict(desc=f"Gaussian-clustered 10M objects, 1M queries, k={_k}",
@@ -234,31 +246,55 @@ def main() -> int:
 
         lo, hi = shard_bounds(wl["n"], world, rank)
     T = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)  # noqa: E731
-    d_ids, d_x, d_y = T(snap.ids[lo:hi]), T(snap.x[lo:hi]), T(snap.y[lo:hi])
     d_qi, d_qx, d_qy = T(qi), T(qx), T(qy)
     cfg = EngineConfig(k=k, region=synth.REGION, device=local)
     stream = torch.cuda.current_stream(dev)
+    delta = bool(wl.get("updates"))
     if world > 1:
         eng = ShardedEngine(cfg, local)
         engine = eng.engine
-        step = lambda out: eng.tick_device(d_ids, d_x, d_y, d_qi, d_qx, d_qy, out=out)  # noqa: E731
     else:
         engine = Engine(cfg)
         engine.set_stream(stream)
-        step = lambda out: engine.tick_device(d_ids, d_x, d_y, d_qi, d_qx, d_qy, out=out)  # noqa: E731
+    if delta:
+        # tick = the tick's U position updates (datasets.py:136-148 carry-forward
+        # over the device-resident snapshot) + the query batch; a few distinct
+        # update batches are cycled (the last update per id wins)
+        n_batches = 4
+        batches = [synth.updates(snap, wl["updates"], t, seed=wl["seed"]) for t in range(n_batches)]
+        U = len(batches[0][0])
+        ulo, uhi = shard_bounds(U, world, rank) if world > 1 else (0, U)
+        d_up = [(T(b[0][ulo:uhi]), T(b[1][ulo:uhi]), T(b[2][ulo:uhi])) for b in batches]
+        if world > 1:
+            eng.load_slices(T(snap.ids[lo:hi]), T(snap.x[lo:hi]), T(snap.y[lo:hi]))
+            step = lambda out, i: eng.update_tick_device(*d_up[i % n_batches], d_qi, d_qx, d_qy,  # noqa: E731
+                                                         out=out)
+        else:
+            engine.load(snap.ids, snap.x, snap.y)
+
+            def step(out, i):
+                engine.update(*d_up[i % n_batches])
+                return engine.query_device(d_qi, d_qx, d_qy, out=out)
+    else:
+        U = wl["n"]
+        d_ids, d_x, d_y = T(snap.ids[lo:hi]), T(snap.x[lo:hi]), T(snap.y[lo:hi])
+        if world > 1:
+            step = lambda out, i: eng.tick_device(d_ids, d_x, d_y, d_qi, d_qx, d_qy, out=out)  # noqa: E731
+        else:
+            step = lambda out, i: engine.tick_device(d_ids, d_x, d_y, d_qi, d_qx, d_qy, out=out)  # noqa: E731
     out = engine.alloc_device_out(nq, dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
 
-    for _ in range(args.warmup):
-        step(out)
+    for i in range(args.warmup):
+        step(out, i)
     torch.cuda.synchronize(dev)
 
     # one extra untimed, instrumented step: T for the roofline
     engine.instrument = True
-    step(out)
+    step(out, 0)
     T_records = engine.last_streamed_records
     engine.instrument = False
-    step(out)
+    step(out, 1)
     torch.cuda.synchronize(dev)
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -272,7 +308,7 @@ def main() -> int:
         for i in range(args.steps):
             flush.zero_()  # L2 flush, outside the timed events
             ev[i][0].record(stream)
-            step(out)
+            step(out, i)
             ev[i][1].record(stream)
             m = engine.last_metrics
             search_us.append(m.t_loop_us)
@@ -292,32 +328,36 @@ def main() -> int:
     e2e = None
     if args.e2e_steps > 0:
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
-        if world == 1:
-            h_in = [pin(snap.ids), pin(snap.x), pin(snap.y), pin(qi), pin(qx), pin(qy)]
-            h_out = (torch.empty(nq, dtype=torch.int64).pin_memory().numpy(),
-                     torch.empty(nq, dtype=torch.int32).pin_memory().numpy(),
-                     torch.empty(nq * k, dtype=torch.int64).pin_memory().numpy(),
-                     torch.empty(nq * k, dtype=torch.float64).pin_memory().numpy())
-            engine.process_tick(*h_in, out=h_out)  # warm the host path
-            secs, nres = [], 0
-            for _ in range(args.e2e_steps):
-                t = time.perf_counter()
-                res = engine.process_tick(*h_in, out=h_out)
-                secs.append(time.perf_counter() - t)
-                nres = len(res.neighbour_ids)
-            h2d = 24 * wl["n"] + 24 * nq
+        h_q = [pin(qi), pin(qx), pin(qy)]
+        h_out = (torch.empty(nq, dtype=torch.int64).pin_memory().numpy(),
+                 torch.empty(nq, dtype=torch.int32).pin_memory().numpy(),
+                 torch.empty(nq * k, dtype=torch.int64).pin_memory().numpy(),
+                 torch.empty(nq * k, dtype=torch.float64).pin_memory().numpy())
+        if delta:
+            h_up = [[pin(a[ulo:uhi]) for a in b] for b in batches]
+            if world == 1:
+                def e2e_step(i):
+                    engine.update(*h_up[i % n_batches])
+                    return engine.query(*h_q, out=h_out)
+            else:
+                e2e_step = lambda i: eng.update_tick(*h_up[i % n_batches], *h_q)  # noqa: E731
+            h2d = 24 * (uhi - ulo) + 24 * nq
         else:
-            h_in = [pin(snap.ids[lo:hi]), pin(snap.x[lo:hi]), pin(snap.y[lo:hi]), pin(qi), pin(qx),
-                    pin(qy)]
-            eng.process_tick(*h_in)
-            secs, nres = [], 0
-            dist.barrier()
-            for _ in range(args.e2e_steps):
-                t = time.perf_counter()
-                res = eng.process_tick(*h_in)
-                secs.append(time.perf_counter() - t)
-                nres = len(res.neighbour_ids)
+            h_snap = [pin(snap.ids[lo:hi]), pin(snap.x[lo:hi]), pin(snap.y[lo:hi])]
+            if world == 1:
+                e2e_step = lambda i: engine.process_tick(*h_snap, *h_q, out=h_out)  # noqa: E731
+            else:
+                e2e_step = lambda i: eng.process_tick(*h_snap, *h_q)  # noqa: E731
             h2d = 24 * (hi - lo) + 24 * nq
+        e2e_step(0)  # warm the host path
+        if world > 1:
+            dist.barrier()
+        secs, nres = [], 0
+        for i in range(args.e2e_steps):
+            t = time.perf_counter()
+            res = e2e_step(i)
+            secs.append(time.perf_counter() - t)
+            nres = len(res.neighbour_ids)
         t_e2e = torch.tensor([statistics.mean(secs)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
@@ -335,7 +375,7 @@ def main() -> int:
     achieved = search_bytes / t_search_s / 1e9
     prof = load_json(os.path.join(ROOT, "profiles", "search_kernel_traffic.json")) or {}
     traffic = prof.get("traffic_bytes_per_launch") if prof.get("workload") == args.workload else None
-    tick_bytes = 24 * wl["n"] + 64 * wl["n"] + 48 * nq + 24 * T_records + 16 * nq * k
+    tick_bytes = 24 * U + 64 * wl["n"] + 48 * nq + 24 * T_records + 16 * nq * k
     m0 = tick_metrics[-1]
 
     line = {
@@ -345,12 +385,17 @@ def main() -> int:
         "config": {
             "workload": wl["desc"], "baseline_config": wl["baseline_idx"], "n_objects": wl["n"],
             "n_queries_per_gpu": nq, "k": k, "th_quad": th, "l_max": 10,
-            "parallelism": f"query shards x{world}, replicated index, NCCL all-gather of "
-                           f"snapshot slices" if world > 1 else "single GPU",
+            "parallelism": (f"query shards x{world}, replicated index, NCCL all-gather of "
+                            f"{'update' if delta else 'snapshot'} slices") if world > 1
+                           else "single GPU",
             "l2": "flushed between steps (256 MB write outside the timed events); "
                   "inputs 264 MB > 126 MB L2",
-            "timed": "Engine.tick_device per step: rebuild decision, index_objects, "
-                     "index_queries, search, emission to device CSR",
+            "timed": ("Engine.update (U device-resident update records) + Engine.query_device per "
+                      "step: update apply, rebuild decision, index_objects, index_queries, search, "
+                      "emission to device CSR" if delta else
+                      "Engine.tick_device per step: rebuild decision, index_objects, "
+                      "index_queries, search, emission to device CSR"),
+            "updates_per_tick": int(U) if delta else None,
         },
         "e2e": e2e,
         "gpu_launches": int(launches),

@@ -103,6 +103,46 @@ class ShardedEngine:
         self.job_distance_evals = total
         self.last_metrics = m
 
+    def load_slices(self, ids_s, x_s, y_s) -> None:
+        """Initial device-resident snapshot from per-rank slices (device
+        tensors): the gathered columns are applied as updates to every rank's
+        empty snapshot (new ids are appended, datasets.py:136-148)."""
+        ids, x, y = all_gather_columns([ids_s, x_s, y_s], self.group)
+        self.engine.update(ids, x, y)
+
+    def update_tick_device(self, u_ids_s, ux_s, uy_s, q_issuer, qx, qy, out=None):
+        """Delta tick: every rank holds 1/G of the tick's position updates
+        (24-byte records); they are all-gathered over NCCL, applied to every
+        rank's replicated snapshot (last update per id wins) and the rank's
+        query shard is answered over it."""
+        ids, x, y = all_gather_columns([u_ids_s, ux_s, uy_s], self.group)
+        self.engine.update(ids, x, y)
+        out = self.engine.query_device(q_issuer, qx, qy, out=out)
+        self._reduce_evals()
+        return out
+
+    def update_tick(self, u_ids_s, ux_s, uy_s, q_issuer, qx, qy) -> TickResult:
+        """Delta tick with host arrays in (this rank's update slice and query
+        shard) and a host TickResult out (this rank's rows, issuer order)."""
+        torch = self.torch
+        dev = self.device
+
+        def h2d(a, dt):
+            return torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev, non_blocking=True)
+
+        out = self.update_tick_device(h2d(u_ids_s, np.int64), h2d(ux_s, np.float64),
+                                      h2d(uy_s, np.float64), h2d(q_issuer, np.int64),
+                                      h2d(qx, np.float64), h2d(qy, np.float64))
+        return self._host_result(out, int(np.asarray(q_issuer).size))
+
+    def _host_result(self, out, nq: int) -> TickResult:
+        nres = out["n_results"]
+        return TickResult(query_ids=out["query_ids"][:nq].cpu().numpy(),
+                          lengths=out["lengths"][:nq].cpu().numpy(),
+                          offsets=out["offsets"][: nq + 1].cpu().numpy(),
+                          neighbour_ids=out["neighbour_ids"][:nres].cpu().numpy(),
+                          distances=out["distances"][:nres].cpu().numpy())
+
     def tick_device(self, ids_s, x_s, y_s, q_issuer, qx, qy, out=None):
         """Snapshot slices + this rank's queries, all CUDA tensors; results
         stay on the device (Engine.tick_device layout)."""
@@ -122,10 +162,4 @@ class ShardedEngine:
 
         out = self.tick_device(h2d(ids_s, np.int64), h2d(x_s, np.float64), h2d(y_s, np.float64),
                                h2d(q_issuer, np.int64), h2d(qx, np.float64), h2d(qy, np.float64))
-        nq = int(np.asarray(q_issuer).size)
-        nres = out["n_results"]
-        lens = out["lengths"][:nq].cpu().numpy()
-        offsets = out["offsets"][: nq + 1].cpu().numpy()
-        return TickResult(query_ids=out["query_ids"][:nq].cpu().numpy(), lengths=lens,
-                          offsets=offsets, neighbour_ids=out["neighbour_ids"][:nres].cpu().numpy(),
-                          distances=out["distances"][:nres].cpu().numpy())
+        return self._host_result(out, int(np.asarray(q_issuer).size))

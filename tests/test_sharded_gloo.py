@@ -91,3 +91,53 @@ def test_two_rank_gather_and_shard_equals_single_process(n, nq):
     assert np.array_equal(np.concatenate([o["nids"] for o in out]), want.neighbour_ids)
     assert np.concatenate([o["dist"] for o in out]).tobytes() == want.distances.tobytes()
     assert out[0]["evals"] == out[1]["evals"] == int(want.lengths.sum())
+
+
+def _delta_worker(rank, world, port, n, nq, k, ret):
+    """ShardedEngine.update_tick_device's host logic on CPU tensors: each rank
+    holds 1/G of the tick's updates, they are all-gathered and applied to the
+    replicated snapshot (last update per id wins, datasets.py:136-148), and
+    the rank answers its query shard over the updated snapshot."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as orc
+        from paper_1412_6170_b200 import synth
+
+        snap = synth.place(n, "uniform", seed=5)
+        rows = []
+        for tick in range(2):
+            uid, ux, uy = synth.updates(snap, 0.1, tick, seed=5)
+            lo, hi = shard_bounds(len(uid), world, rank)
+            g_id, g_x, g_y = all_gather_columns([torch.from_numpy(uid[lo:hi].copy()),
+                                                 torch.from_numpy(ux[lo:hi].copy()),
+                                                 torch.from_numpy(uy[lo:hi].copy())])
+            assert np.array_equal(g_id.numpy(), uid)
+            synth.apply_updates(snap, g_id.numpy(), g_x.numpy(), g_y.numpy())
+            qi, qx, qy = synth.queries(snap, nq, seed=tick)
+            sel = shard_queries(qi, world, rank)
+            res = orc.brute_force_knn(snap.ids, snap.x, snap.y, qi[sel], qx[sel], qy[sel], k)
+            rows.append((res.query_ids, res.neighbour_ids, res.distances))
+        ret[rank] = rows
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_update_gather_equals_single_process():
+    world, n, nq, k = 2, 2500, 300, 5
+    port = _free_port()
+    with mp.Manager() as mgr:
+        ret = mgr.dict()
+        mp.spawn(_delta_worker, args=(world, port, n, nq, k, ret), nprocs=world, join=True)
+        out = [ret[r] for r in range(world)]
+    from oracle import oracle as orc
+    from paper_1412_6170_b200 import synth
+
+    snap = synth.place(n, "uniform", seed=5)
+    for tick in range(2):
+        synth.apply_updates(snap, *synth.updates(snap, 0.1, tick, seed=5))
+        qi, qx, qy = synth.queries(snap, nq, seed=tick)
+        want = orc.brute_force_knn(snap.ids, snap.x, snap.y, qi, qx, qy, k)
+        assert np.array_equal(np.concatenate([o[tick][0] for o in out]), want.query_ids)
+        assert np.array_equal(np.concatenate([o[tick][1] for o in out]), want.neighbour_ids)
+        assert np.concatenate([o[tick][2] for o in out]).tobytes() == want.distances.tobytes()
