@@ -506,13 +506,15 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
                      std::chrono::steady_clock::now() - t_start)
                      .count();
   if (a.prof) {  // profiling only (MKNN_PROF=1)
-    unsigned long long pv[8];
+    unsigned long long pv[10];
     MKNN_CUDA_OK(cudaMemcpy(pv, h->prof, sizeof(pv), cudaMemcpyDeviceToHost));
     fprintf(stderr,
             "[mknn prof] per query: own chunks %.2f/%.2f, exp leaves %.2f, exp chunks %.2f/%.2f, "
-            "admitted %.2f, inserts %.2f, sort-merges %.2f\n",
+            "admitted %.2f, inserts %.2f, sort-merges %.2f; exp visits without scans %.2f, "
+            "with admissions %.2f\n",
             (double)pv[0] / nq, (double)pv[5] / nq, (double)pv[4] / nq, (double)pv[1] / nq,
-            (double)pv[6] / nq, (double)pv[7] / nq, (double)pv[2] / nq, (double)pv[3] / nq);
+            (double)pv[6] / nq, (double)pv[7] / nq, (double)pv[2] / nq, (double)pv[3] / nq,
+            (double)pv[8] / nq, (double)pv[9] / nq);
   }
   if (met) *met = m;
   return 0;

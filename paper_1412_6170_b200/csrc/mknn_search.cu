@@ -243,7 +243,8 @@ __device__ __forceinline__ void list_kth(const List<KPL>& L, int k, double& kd, 
 // Profiling counters (MKNN_PROF=1; nullptr otherwise): what the warps did.
 enum {
   PROF_OWN_CHUNKS_SCANNED, PROF_EXP_CHUNKS_SCANNED, PROF_INSERTS, PROF_SORT_MERGES,
-  PROF_EXP_LEAF_VISITS, PROF_OWN_CHUNKS_TOTAL, PROF_EXP_CHUNKS_TOTAL, PROF_ADMITTED, PROF_N
+  PROF_EXP_LEAF_VISITS, PROF_OWN_CHUNKS_TOTAL, PROF_EXP_CHUNKS_TOTAL, PROF_ADMITTED,
+  PROF_EXP_VISITS_NO_SCAN, PROF_EXP_VISITS_ADMITTING, PROF_N
 };
 #ifndef MKNN_PROFILE
 #define MKNN_PROFILE 0
@@ -349,6 +350,9 @@ __device__ __forceinline__ void visit_leaf(List<KPL>& L, int k, int leaf, double
   const int c0 = __ldg(&a.chunk_start[leaf]), c1 = __ldg(&a.chunk_start[leaf + 1]);
   prof_add(a.prof, own ? PROF_OWN_CHUNKS_TOTAL : PROF_EXP_CHUNKS_TOTAL, c1 - c0, lane);
   if (!own) prof_add(a.prof, PROF_EXP_LEAF_VISITS, 1, lane);
+  bool scanned = false, admitted = false;  // profiling only
+  (void)scanned;
+  (void)admitted;
   double kd;
   long long ki;
   list_kth<KPL>(L, k, kd, ki);
@@ -369,8 +373,16 @@ __device__ __forceinline__ void visit_leaf(List<KPL>& L, int k, int leaf, double
       const bool v = cb + lane < min(cb + CHUNK, oe);
       const StoreRec r = load_rec(a.obj, cb + lane, v);
       prof_add(a.prof, own ? PROF_OWN_CHUNKS_SCANNED : PROF_EXP_CHUNKS_SCANNED, 1, lane);
-      if (scan_rec<KPL>(L, kd, ki, v, r, qx, qy, me, lane, a.prof)) list_kth<KPL>(L, k, kd, ki);
+      scanned = true;
+      if (scan_rec<KPL>(L, kd, ki, v, r, qx, qy, me, lane, a.prof)) {
+        list_kth<KPL>(L, k, kd, ki);
+        admitted = true;
+      }
     }
+  }
+  if (!own) {
+    prof_add(a.prof, PROF_EXP_VISITS_NO_SCAN, !scanned, lane);
+    prof_add(a.prof, PROF_EXP_VISITS_ADMITTING, admitted, lane);
   }
 }
 
