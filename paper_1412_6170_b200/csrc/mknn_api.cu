@@ -571,16 +571,42 @@ int ensure_out_dev(mknn_engine* h, int64_t nq) {
 }
 
 // host-output tick over device-resident inputs (mknn_tick / mknn_query)
+// device address of a pinned, mapped host buffer (nullptr if it is not one)
+void* device_view(void* host) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, host) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
 int host_out_tick(mknn_engine* h, int64_t n, const long long* ids, const double* x, const double* y,
                   int64_t nq, const long long* qi, const double* qx, const double* qy,
                   int64_t* out_qids, int32_t* out_len, int64_t* out_nids, double* out_dist,
                   mknn_metrics* metrics, std::chrono::steady_clock::time_point t0) {
   int rc;
   if ((rc = ensure_out_dev(h, nq))) return h->set_err(rc);
+  // Pinned, device-mapped host outputs (cudaHostAlloc / torch pin_memory):
+  // the search writes its rows straight over PCIe while it runs, so the
+  // result transfer overlaps the kernel instead of following it.
+  void* mq = device_view(out_qids);
+  void* ml = device_view(out_len);
+  void* mn = device_view(out_nids);
+  void* md = device_view(out_dist);
+  const bool mapped = nq > 0 && mq && ml && mn && md;
   DevOut o{h->out_qids, h->out_len, h->offsets, h->c_nids, h->c_dist};
+  if (mapped) o = DevOut{(long long*)mq, (int32_t*)ml, h->offsets, (long long*)mn, (double*)md};
   mknn_metrics m{};
   if ((rc = core_tick(h, n, ids, x, y, nq, qi, qx, qy, o, &m, t0))) return rc;
   cudaStream_t s = h->stream;
+  if (mapped) {
+    m.t_total_us = std::chrono::duration_cast<std::chrono::microseconds>(
+                       std::chrono::steady_clock::now() - t0)
+                       .count();
+    if (metrics) *metrics = m;
+    return 0;
+  }
   if (nq) {
     MKNN_CUDA_OK(cudaMemcpyAsync(out_qids, h->out_qids, sizeof(int64_t) * nq, cudaMemcpyDeviceToHost, s));
     MKNN_CUDA_OK(cudaMemcpyAsync(out_len, h->out_len, sizeof(int32_t) * nq, cudaMemcpyDeviceToHost, s));

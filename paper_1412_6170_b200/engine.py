@@ -277,8 +277,12 @@ class Engine:
         return tm
 
     def _result(self, qids, lens, nids, dist, n_results) -> TickResult:
-        offsets = np.zeros(len(lens) + 1, np.int64)
-        np.cumsum(lens, out=offsets[1:])
+        k = self.config.k
+        if n_results == len(lens) * k:  # every row full: the CSR is the padded rows
+            offsets = np.arange(0, (len(lens) + 1) * k, k, dtype=np.int64)
+        else:
+            offsets = np.zeros(len(lens) + 1, np.int64)
+            np.cumsum(lens, out=offsets[1:])
         return TickResult(query_ids=qids, lengths=lens, offsets=offsets,
                           neighbour_ids=nids[:n_results], distances=dist[:n_results])
 

@@ -270,3 +270,23 @@ def test_cell_borders_match_reference_encoding(lo, width):
         np.testing.assert_array_equal(ce, want_st["cell_end"])
         assert eng.last_metrics.clamped_objects == want_st["clamped"]
     assert_same(res, orc.brute_force_knn(ids, xs, ys, ids[sel], xs[sel], ys[sel], 6))
+
+
+@pytest.mark.parametrize("n,k", [(5000, 16), (20, 32)])
+def test_pinned_host_outputs_written_in_place(n, k):
+    """Pinned (device-mapped) host output buffers are written by the search
+    kernel directly; full rows and short rows (n - 1 < k) both match."""
+    rng = np.random.default_rng(n)
+    x = rng.uniform(0, 100, n)
+    y = rng.uniform(0, 100, n)
+    ids = np.arange(n, dtype=np.int64) * 3
+    nq = min(n, 700)
+    sel = rng.choice(n, nq, replace=False)
+    qi, qx, qy = ids[sel], x[sel], y[sel]
+    pin = lambda shape, dt: torch.empty(shape, dtype=dt).pin_memory().numpy()  # noqa: E731
+    out = (pin(nq, torch.int64), pin(nq, torch.int32), pin(nq * k, torch.int64),
+           pin(nq * k, torch.float64))
+    with Engine(EngineConfig(k=k, region=Rect.square(100.0), th_quad=24)) as eng:
+        for _ in range(2):
+            res = eng.process_tick(ids, x, y, qi, qx, qy, out=out)
+            assert_same(res, orc.brute_force_knn(ids, x, y, qi, qx, qy, k))
