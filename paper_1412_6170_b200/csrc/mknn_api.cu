@@ -158,6 +158,11 @@ int64_t us_between(cudaEvent_t a, cudaEvent_t b) {
 
 }  // namespace
 
+// host-output ticks of >= SLICE_MIN_QUERIES queries search in N_SLICES
+// result-row slices whose copies to the host overlap the next slice
+constexpr int N_SLICES = 4;
+constexpr int64_t SLICE_MIN_QUERIES = 65536;
+
 struct mknn_engine {
   mknn_config cfg{};
   Region r{};
@@ -170,6 +175,9 @@ struct mknn_engine {
   bool have_index = false;
   bool last_tick_ok = false;
   int issuer_bits = -1;        // issuer-id bits of the last tick (plans the row sort)
+  cudaStream_t copy_stream = nullptr;  // result slices device -> host
+  cudaEvent_t slice_ev[N_SLICES] = {};
+  bool rows_in_host = false;   // the sliced host tick already delivered qids/len/rows
   bool retry_rebuild = false;  // false: the store's sub-cell counters may be dirty
   int32_t h_l_deep = 0;
   int64_t h_n_leaves = 0, h_overfull = 0, h_n_build = 0, h_n_sub = 0;
@@ -234,6 +242,27 @@ bool should_rebuild(const std::vector<int64_t>& c, int window, double factor) {
 
 // ---------------------------------------------------------------- core tick
 namespace {
+
+// Host destinations of a host-output tick: when set, the search runs in
+// slices of consecutive result rows and each slice's rows are copied to the
+// host (on the copy stream) while the next slice computes.
+struct HostSink {
+  int64_t* qids;
+  int32_t* len;
+  int64_t* nids;
+  double* dist;
+};
+
+__global__ void k_slice_keys(const uint32_t* __restrict__ order, const uint32_t* __restrict__ row,
+                             int64_t nq, int n_slices, uint64_t* __restrict__ keys,
+                             uint32_t* __restrict__ vals) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nq) {
+    const uint32_t q = order[i];
+    keys[i] = (uint64_t)row[q] * (uint64_t)n_slices / (uint64_t)nq;
+    vals[i] = q;
+  }
+}
 
 struct DevOut {
   long long* qids;    // [nq] or nullptr
@@ -311,7 +340,8 @@ int refresh_index_info(mknn_engine* h) {
 int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double* x,
                    const double* y, int64_t nq, const long long* qi, const double* qx,
                    const double* qy, const DevOut& o, mknn_metrics* met,
-                   std::chrono::steady_clock::time_point t_start, bool force_rebuild, bool* retry) {
+                   std::chrono::steady_clock::time_point t_start, bool force_rebuild, bool* retry,
+                   const HostSink* sink) {
   *retry = false;
   const int k = h->cfg.k;
   cudaStream_t s = h->stream;
@@ -414,7 +444,48 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
     a.task_count = h->tk_cnt;
     a.task_cap = h->cap_tk;
   }
-  if ((rc = search_launch(a, s))) return h->set_err(rc);
+  const bool sliced = sink && nq >= SLICE_MIN_QUERIES;
+  h->rows_in_host = false;
+  if (!sliced) {
+    if ((rc = search_launch(a, s))) return h->set_err(rc);
+  } else {
+    // stable partition of the leaf-grouped order by result-row slice: slice
+    // j holds rows [ceil(j nq / S), ceil((j + 1) nq / S)), each slice keeps
+    // the leaf order (one 8-bit radix pass), then slice j's rows are copied
+    // out while slice j + 1 searches
+    MKNN_LAUNCH k_slice_keys<<<(unsigned)((nq + 255) / 256), 256, 0, s>>>(
+        h->dq.order, h->dq.row, nq, N_SLICES, h->dq.keys, h->dq.vals);
+    bool alt = false;
+    if ((rc = radix_sort_pairs_u64(h->dq.keys, h->dq.vals, h->dq.keys_alt, h->dq.vals_alt, nq, 8,
+                                   h->scratch.p, s, &alt)))
+      return h->set_err(rc);
+    const uint32_t* sorder = alt ? h->dq.vals_alt : h->dq.vals;
+    if (o.qids) {  // issuer-ordered query ids are final already
+      MKNN_CUDA_OK(cudaEventRecord(h->ev[6], s));
+      MKNN_CUDA_OK(cudaStreamWaitEvent(h->copy_stream, h->ev[6], 0));
+      MKNN_CUDA_OK(cudaMemcpyAsync(sink->qids, o.qids, sizeof(int64_t) * nq, cudaMemcpyDeviceToHost,
+                                   h->copy_stream));
+    }
+    for (int j = 0; j < N_SLICES; j++) {
+      const int64_t r0 = (j * nq + N_SLICES - 1) / N_SLICES;
+      const int64_t r1 = ((j + 1) * nq + N_SLICES - 1) / N_SLICES;
+      if (r1 <= r0) continue;
+      SearchArgs aj = a;
+      aj.q_order = sorder + r0;
+      aj.nq = r1 - r0;
+      aj.stats = h->stats + r0;
+      if ((rc = search_launch(aj, s))) return h->set_err(rc);
+      MKNN_CUDA_OK(cudaEventRecord(h->slice_ev[j], s));
+      MKNN_CUDA_OK(cudaStreamWaitEvent(h->copy_stream, h->slice_ev[j], 0));
+      cudaStream_t c = h->copy_stream;
+      MKNN_CUDA_OK(cudaMemcpyAsync(sink->len + r0, o.len + r0, sizeof(int32_t) * (r1 - r0),
+                                   cudaMemcpyDeviceToHost, c));
+      MKNN_CUDA_OK(cudaMemcpyAsync(sink->nids + r0 * k, o.nids + r0 * k,
+                                   sizeof(int64_t) * (r1 - r0) * k, cudaMemcpyDeviceToHost, c));
+      MKNN_CUDA_OK(cudaMemcpyAsync(sink->dist + r0 * k, o.dist + r0 * k,
+                                   sizeof(double) * (r1 - r0) * k, cudaMemcpyDeviceToHost, c));
+    }
+  }
   MKNN_CUDA_OK(cudaEventRecord(h->ev[4], s));
   m.streamed_records = -1;
   if (instr) {
@@ -448,6 +519,10 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
   int64_t total = 0;
   MKNN_CUDA_OK(cudaMemcpyAsync(&total, o.offsets + nq, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   MKNN_CUDA_OK(cudaStreamSynchronize(s));
+  if (sliced) {
+    MKNN_CUDA_OK(cudaStreamSynchronize(h->copy_stream));
+    h->rows_in_host = total == nq * (int64_t)k;  // short rows: the caller copies the CSR
+  }
   if (nq) {
     // the issuer sort was planned from the previous tick's id range: if this
     // tick's range needs more bits the row order is wrong -> redo the tick
@@ -522,12 +597,14 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
 
 int core_tick(mknn_engine* h, int64_t n, const long long* ids, const double* x, const double* y,
               int64_t nq, const long long* qi, const double* qx, const double* qy, const DevOut& o,
-              mknn_metrics* met, std::chrono::steady_clock::time_point t_start) {
+              mknn_metrics* met, std::chrono::steady_clock::time_point t_start,
+              const HostSink* sink = nullptr) {
   bool retry = false;
-  int rc = core_tick_once(h, n, ids, x, y, nq, qi, qx, qy, o, met, t_start, false, &retry);
+  int rc = core_tick_once(h, n, ids, x, y, nq, qi, qx, qy, o, met, t_start, false, &retry, sink);
   if (rc || !retry) return rc;
   // issuer bits now measured exactly: the second pass cannot retry
-  rc = core_tick_once(h, n, ids, x, y, nq, qi, qx, qy, o, met, t_start, h->retry_rebuild, &retry);
+  rc = core_tick_once(h, n, ids, x, y, nq, qi, qx, qy, o, met, t_start, h->retry_rebuild, &retry,
+                      sink);
   if (!rc && retry) return fail_msg(E_CUDA, "issuer order retry did not converge");
   return rc;
 }
@@ -571,36 +648,18 @@ int ensure_out_dev(mknn_engine* h, int64_t nq) {
 }
 
 // host-output tick over device-resident inputs (mknn_tick / mknn_query)
-// device address of a pinned, mapped host buffer (nullptr if it is not one)
-void* device_view(void* host) {
-  cudaPointerAttributes at{};
-  if (cudaPointerGetAttributes(&at, host) != cudaSuccess) {
-    cudaGetLastError();
-    return nullptr;
-  }
-  return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
-}
-
 int host_out_tick(mknn_engine* h, int64_t n, const long long* ids, const double* x, const double* y,
                   int64_t nq, const long long* qi, const double* qx, const double* qy,
                   int64_t* out_qids, int32_t* out_len, int64_t* out_nids, double* out_dist,
                   mknn_metrics* metrics, std::chrono::steady_clock::time_point t0) {
   int rc;
   if ((rc = ensure_out_dev(h, nq))) return h->set_err(rc);
-  // Pinned, device-mapped host outputs (cudaHostAlloc / torch pin_memory):
-  // the search writes its rows straight over PCIe while it runs, so the
-  // result transfer overlaps the kernel instead of following it.
-  void* mq = device_view(out_qids);
-  void* ml = device_view(out_len);
-  void* mn = device_view(out_nids);
-  void* md = device_view(out_dist);
-  const bool mapped = nq > 0 && mq && ml && mn && md;
   DevOut o{h->out_qids, h->out_len, h->offsets, h->c_nids, h->c_dist};
-  if (mapped) o = DevOut{(long long*)mq, (int32_t*)ml, h->offsets, (long long*)mn, (double*)md};
+  const HostSink sink{out_qids, out_len, out_nids, out_dist};
   mknn_metrics m{};
-  if ((rc = core_tick(h, n, ids, x, y, nq, qi, qx, qy, o, &m, t0))) return rc;
+  if ((rc = core_tick(h, n, ids, x, y, nq, qi, qx, qy, o, &m, t0, &sink))) return rc;
   cudaStream_t s = h->stream;
-  if (mapped) {
+  if (h->rows_in_host) {
     m.t_total_us = std::chrono::duration_cast<std::chrono::microseconds>(
                        std::chrono::steady_clock::now() - t0)
                        .count();
@@ -764,6 +823,10 @@ int mknn_create(const mknn_config* cfg, mknn_engine** out) {
   if (!rc && cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking) != cudaSuccess) rc = E_CUDA;
   for (int i = 0; i < 8 && !rc; i++)
     if (cudaEventCreate(&h->ev[i]) != cudaSuccess) rc = E_CUDA;
+  for (int i = 0; i < N_SLICES && !rc; i++)
+    if (cudaEventCreateWithFlags(&h->slice_ev[i], cudaEventDisableTiming) != cudaSuccess) rc = E_CUDA;
+  if (!rc && cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
+    rc = E_CUDA;
   if (rc) {
     mknn_destroy(h);
     return rc;
@@ -792,6 +855,9 @@ void mknn_destroy(mknn_engine* h) {
   h->scratch.release();
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : h->slice_ev)
+    if (e) cudaEventDestroy(e);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
 }

@@ -290,3 +290,43 @@ def test_pinned_host_outputs_written_in_place(n, k):
         for _ in range(2):
             res = eng.process_tick(ids, x, y, qi, qx, qy, out=out)
             assert_same(res, orc.brute_force_knn(ids, x, y, qi, qx, qy, k))
+
+
+def test_sliced_host_tick_equals_device_tick():
+    """Host ticks of >= 64K queries search in result-row slices whose copies
+    overlap the next slice; the CSR must equal the device-resident tick's and
+    a brute-force sample."""
+    snap = synth.place(200_000, "gaussian", seed=8, hotspots=6, sigma=900.0)
+    qi, qx, qy = synth.queries(snap, 90_000, seed=8)
+    with Engine(EngineConfig(k=12, region=synth.REGION)) as eng:
+        res = eng.process_tick(snap.ids, snap.x, snap.y, qi, qx, qy)
+        T = lambda a: torch.as_tensor(np.ascontiguousarray(a), device="cuda")  # noqa: E731
+        out = eng.tick_device(T(snap.ids), T(snap.x), T(snap.y), T(qi), T(qx), T(qy))
+        nres = out["n_results"]
+        np.testing.assert_array_equal(res.query_ids, out["query_ids"][:len(qi)].cpu().numpy())
+        np.testing.assert_array_equal(res.neighbour_ids, out["neighbour_ids"][:nres].cpu().numpy())
+        assert res.distances.tobytes() == out["distances"][:nres].cpu().numpy().tobytes()
+    rows = np.sort(np.random.default_rng(0).choice(len(qi), 300, replace=False))
+    order = np.argsort(qi, kind="stable")
+    want = orc.brute_force_knn(snap.ids, snap.x, snap.y, qi[order[rows]], qx[order[rows]],
+                               qy[order[rows]], 12)
+    for j, r in enumerate(rows):
+        a, b = res.offsets[r], res.offsets[r + 1]
+        np.testing.assert_array_equal(res.neighbour_ids[a:b],
+                                      want.neighbour_ids[want.offsets[j]:want.offsets[j + 1]])
+
+
+def test_sliced_host_tick_short_rows():
+    """Sliced host tick whose rows are short (fewer objects than k): the
+    compacted CSR replaces the row copies."""
+    rng = np.random.default_rng(3)
+    n, nq, k = 20, 70_000, 32
+    x = rng.uniform(0, 10, n)
+    y = rng.uniform(0, 10, n)
+    ids = np.arange(n, dtype=np.int64)
+    qi = rng.integers(0, 40, nq).astype(np.int64)  # issuers in and out of the snapshot
+    qx = rng.uniform(0, 10, nq)
+    qy = rng.uniform(0, 10, nq)
+    with Engine(EngineConfig(k=k, region=Rect.square(10.0), th_quad=4)) as eng:
+        res = eng.process_tick(ids, x, y, qi, qx, qy)
+    assert_same(res, orc.brute_force_knn(ids, x, y, qi, qx, qy, k))
