@@ -129,34 +129,45 @@ __global__ void k_leaf_table(const int32_t* __restrict__ flags, const int32_t* _
 }
 
 
+// Per deepest cell, everything a point needs to get its leaf and store key
+// in one gather (built at rebuild): bits 0-31 sub_base of the cell's leaf,
+// 32-37 the shift that brings the point's level-16 code to the leaf's
+// sub-cell level, 38-41 the sub-cell bits, 42-63 the leaf ordinal.
+__global__ void k_cell_info(const int32_t* __restrict__ z_map, const int32_t* __restrict__ scalars,
+                            const uint8_t* __restrict__ leaf_level,
+                            const uint8_t* __restrict__ sub_bits,
+                            const int32_t* __restrict__ sub_base, int64_t ncap,
+                            unsigned long long* __restrict__ info) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int l_deep = scalars[0];
+  if (c >= ((int64_t)1 << (2 * l_deep)) || c >= ncap) return;
+  const int leaf = z_map[c];
+  const int sb = sub_bits[leaf];
+  const int shift = 2 * (16 - leaf_level[leaf]) - sb;
+  info[c] = (unsigned long long)(uint32_t)sub_base[leaf] | ((unsigned long long)shift << 32) |
+            ((unsigned long long)sb << 38) | ((unsigned long long)leaf << 42);
+}
+
 // Per point: the leaf (encode at l_deep -> z_map, quadindex.py:196-199;
 // engine.py:206) and the sub-cell key sub_base[leaf] + sub, where sub is the
 // point's Morton code s levels below the leaf's level.  The l_deep code is
 // the prefix of the level-16 code (floor(t * 2^16) >> d == floor(t * 2^(16-d))
-// for the same t, geometry.py:108-112), so both come from one normalisation.
+// for the same t, geometry.py:108-112), so both come from one normalisation,
+// and the cell table turns them into the leaf and the key with one gather.
 __device__ __forceinline__ void point_key(double xi, double yi, const Region& r, int l_deep,
-                                          const int32_t* __restrict__ z_map,
-                                          const uint8_t* __restrict__ leaf_level,
-                                          const uint8_t* __restrict__ sub_bits,
-                                          const int32_t* __restrict__ sub_base, uint32_t& leaf,
-                                          uint32_t& key) {
+                                          const unsigned long long* __restrict__ info,
+                                          uint32_t& leaf, uint32_t& key) {
   const uint32_t f = encode16(xi, yi, r);
-  leaf = (uint32_t)__ldg(&z_map[f >> (2 * (16 - l_deep))]);
-  const int sb = __ldg(&sub_bits[leaf]);
-  uint32_t sub = 0;
-  if (sb) {
-    const int lvl = __ldg(&leaf_level[leaf]);
-    sub = (f >> (2 * (16 - lvl) - sb)) & ((1u << sb) - 1u);
-  }
-  key = (uint32_t)__ldg(&sub_base[leaf]) + sub;
+  const unsigned long long e = __ldg(&info[f >> (2 * (16 - l_deep))]);
+  const int shift = (int)((e >> 32) & 63u), sb = (int)((e >> 38) & 15u);
+  leaf = (uint32_t)(e >> 42);
+  key = (uint32_t)e + ((f >> shift) & ((1u << sb) - 1u));
 }
 
 __global__ void k_point_keys(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                              Region r, const int32_t* __restrict__ scalars,
-                             const int32_t* __restrict__ z_map,
-                             const uint8_t* __restrict__ leaf_level,
-                             const uint8_t* __restrict__ sub_bits,
-                             const int32_t* __restrict__ sub_base, uint32_t* __restrict__ leaf_out,
+                             const unsigned long long* __restrict__ info,
+                             uint32_t* __restrict__ leaf_out,
                              uint32_t* __restrict__ key_out, int32_t* __restrict__ cnt,
                              unsigned long long* clamped, int bshift,
                              int32_t* __restrict__ bucket_cnt) {
@@ -186,7 +197,7 @@ __global__ void k_point_keys(const double* __restrict__ x, const double* __restr
         // geometry.py:215-220 count_outside
         out += (xi[u] < r.x_lo) | (xi[u] > r.x_hi) | (yi[u] < r.y_lo) | (yi[u] > r.y_hi);
         uint32_t leaf, key;
-        point_key(xi[u], yi[u], r, l_deep, z_map, leaf_level, sub_bits, sub_base, leaf, key);
+        point_key(xi[u], yi[u], r, l_deep, info, leaf, key);
         if (leaf_out) leaf_out[i] = leaf;
         key_out[i] = key;
         atomicAdd(&cnt[key], 1);
@@ -416,6 +427,7 @@ int index_alloc(DevIndex& ix, int l_max, int th_quad) {
   MKNN_CUDA_OK(cudaMalloc(&ix.scalars, sizeof(int32_t) * 8));
   MKNN_CUDA_OK(cudaMalloc(&ix.leaf_sub_bits, ncap));
   MKNN_CUDA_OK(cudaMalloc(&ix.leaf_sub_base, sizeof(int32_t) * (ncap + 1)));
+  MKNN_CUDA_OK(cudaMalloc(&ix.cell_info, sizeof(unsigned long long) * ncap));
   return 0;
 }
 
@@ -432,6 +444,7 @@ void index_free(DevIndex& ix) {
   cudaFree(ix.scalars);
   cudaFree(ix.leaf_sub_bits);
   cudaFree(ix.leaf_sub_base);
+  cudaFree(ix.cell_info);
   ix = DevIndex{};
 }
 
@@ -472,6 +485,9 @@ int index_build(DevIndex& ix, const Region& r, const double* x, const double* y,
   rc = exclusive_scan_i32(flags, ix.leaf_sub_base, ncap, scratch, s);
   if (rc) return rc;
   MKNN_LAUNCH k_store_scalar<<<1, 1, 0, s>>>(ix.scalars, ix.leaf_sub_base, ncap);
+  MKNN_LAUNCH k_cell_info<<<blocks_for(ncap), TPB, 0, s>>>(ix.z_map, ix.scalars, ix.leaf_level,
+                                                          ix.leaf_sub_bits, ix.leaf_sub_base, ncap,
+                                                          ix.cell_info);
   MKNN_CUDA_OK(cudaGetLastError());
   // n_build for should_rebuild bookkeeping
   int32_t nb = (int32_t)std::min<int64_t>(n, 0x7fffffff);
@@ -525,8 +541,8 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
   MKNN_CUDA_OK(cudaMemsetAsync(st.cursor, 0, sizeof(int32_t) * PT_BUCKETS, s));
   if (n > 0)
     MKNN_LAUNCH k_point_keys<<<grid_stride_blocks(n), TPB, 0, s>>>(
-        x, y, n, r, ix.scalars, ix.z_map, ix.leaf_level, ix.leaf_sub_bits, ix.leaf_sub_base,
-        nullptr, st.key, st.cnt, dev_clamped, bshift, st.cursor);
+        x, y, n, r, ix.scalars, ix.cell_info, nullptr, st.key, st.cnt, dev_clamped, bshift,
+        st.cursor);
   MKNN_CUDA_OK(cudaGetLastError());
   MKNN_LAUNCH k_bucket_scan<<<1, PT_BUCKETS, 0, s>>>(st.cursor, st.bstart, st.cursor);
   if (n > 0) {
@@ -568,8 +584,7 @@ int queries_index(DevQueries& dq, DevStore& st, const DevIndex& ix, const Region
   *bits_used = 0;
   if (nq == 0) return 0;
   MKNN_LAUNCH k_point_keys<<<grid_stride_blocks(nq), TPB, 0, s>>>(
-      qx, qy, nq, r, ix.scalars, ix.z_map, ix.leaf_level, ix.leaf_sub_bits, ix.leaf_sub_base,
-      dq.leaf, dq.qkey, st.cnt, nullptr, 0, nullptr);
+      qx, qy, nq, r, ix.scalars, ix.cell_info, dq.leaf, dq.qkey, st.cnt, nullptr, 0, nullptr);
   MKNN_CUDA_OK(cudaGetLastError());
   int rc = exclusive_scan_i32(st.cnt, st.kstart, n_sub, scratch, s);
   if (rc) return rc;

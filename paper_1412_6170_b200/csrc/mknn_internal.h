@@ -62,6 +62,7 @@ struct DevIndex {
   // leaf's build count), leaf l owns sub-cell keys [sub_base[l], sub_base[l+1])
   uint8_t* leaf_sub_bits = nullptr;  // 2*s
   int32_t* leaf_sub_base = nullptr;  // 4^l_max + 1
+  unsigned long long* cell_info = nullptr;  // per deepest cell: sub_base | shift | bits | leaf
   int l_max = 0;
   int th_quad = 0;
 };

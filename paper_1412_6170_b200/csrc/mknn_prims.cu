@@ -150,10 +150,20 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_lookback(
   }
   __syncthreads();
   ex += tile_excl;
+  TO o[SCAN_ITEMS];
 #pragma unroll
   for (int i = 0; i < SCAN_ITEMS; i++) {
-    if (base + i < n) out[base + i] = (TO)ex;
+    o[i] = (TO)ex;
     ex += v[i];
+  }
+  constexpr int VEC = 16 / sizeof(TO);  // elements per 16-byte store
+  if (base + SCAN_ITEMS <= n && (reinterpret_cast<uintptr_t>(out + base) & 15) == 0) {
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; i += VEC) *reinterpret_cast<int4*>(&out[base + i]) = *reinterpret_cast<int4*>(&o[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; i++)
+      if (base + i < n) out[base + i] = o[i];
   }
   if (tile == n_tiles - 1 && threadIdx.x == blockDim.x - 1) out[n] = (TO)ex;
 }
