@@ -377,6 +377,7 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
     m.rebuild_flag = 1;
     if ((rc = refresh_index_info(h))) return h->set_err(rc);  // leaf count sizes the store tables
   }
+  h->st.chunk = chunk_for_k(k);
   if ((rc = store_reserve(h->st, h->h_n_sub, h->h_n_leaves, n))) return h->set_err(rc);
   if (!h->last_tick_ok) h->st.dirty = true;
   h->last_tick_ok = false;

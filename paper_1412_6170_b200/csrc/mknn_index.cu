@@ -313,25 +313,25 @@ __global__ void k_q_scatter(int64_t nq, const uint32_t* __restrict__ key,
 
 // leaf ranges from the sub-cell starts: cell_start[l] and chunks per leaf
 __global__ void k_leaf_ranges(const int32_t* __restrict__ kstart, const int32_t* __restrict__ sub_base,
-                              int64_t n_leaves, int32_t* __restrict__ cell_start,
+                              int64_t n_leaves, int chunk, int32_t* __restrict__ cell_start,
                               int32_t* __restrict__ nch) {
   const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (l <= n_leaves) {
     const int32_t b = kstart[sub_base[l]];
     cell_start[l] = b;
-    if (l < n_leaves) nch[l] = (kstart[sub_base[l + 1]] - b + CHUNK - 1) / CHUNK;
+    if (l < n_leaves) nch[l] = (kstart[sub_base[l + 1]] - b + chunk - 1) / chunk;
   }
 }
 
 // per leaf: the object range of each of its chunks
 __global__ void k_chunk_ranges(const int32_t* __restrict__ cell_start,
                                const int32_t* __restrict__ chunk_start, int64_t n_leaves,
-                               int2* __restrict__ crange) {
+                               int chunk, int2* __restrict__ crange) {
   const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (l < n_leaves) {
     const int b = cell_start[l], e = cell_start[l + 1];
     int c = chunk_start[l];
-    for (int o = b; o < e; o += CHUNK, c++) crange[c] = make_int2(o, min(o + CHUNK, e));
+    for (int o = b; o < e; o += chunk, c++) crange[c] = make_int2(o, min(o + chunk, e));
   }
 }
 
@@ -508,7 +508,7 @@ int store_reserve(DevStore& st, int64_t n_sub, int64_t n_leaves, int64_t n) {
     st.cap_sub = c;
     st.dirty = true;
   }
-  const int64_t nbox = n / CHUNK + n_leaves + 1;
+  const int64_t nbox = n / (MAX_CHUNK / 2) + n_leaves + 1;
   if (!st.cursor) {
     MKNN_CUDA_OK(cudaMalloc(&st.cursor, sizeof(int32_t) * (PT_BUCKETS + 1)));
     MKNN_CUDA_OK(cudaMalloc(&st.bstart, sizeof(int32_t) * (PT_BUCKETS + 1)));
@@ -557,14 +557,15 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
                                                                      st.obj);
   MKNN_CUDA_OK(cudaGetLastError());
   MKNN_LAUNCH k_leaf_ranges<<<blocks_for(n_leaves + 1), TPB, 0, s>>>(st.kstart, ix.leaf_sub_base,
-                                                                    n_leaves, st.cell_start, st.nch);
+                                                                    n_leaves, st.chunk, st.cell_start,
+                                                                    st.nch);
   MKNN_CUDA_OK(cudaGetLastError());
   rc = exclusive_scan_i32(st.nch, st.chunk_start, n_leaves, scratch, s);
   if (rc) return rc;
   if (n > 0) {
     MKNN_LAUNCH k_chunk_ranges<<<blocks_for(n_leaves), TPB, 0, s>>>(st.cell_start, st.chunk_start,
-                                                                   n_leaves, st.crange);
-    const int64_t maxc = n / CHUNK + n_leaves + 1;
+                                                                   n_leaves, st.chunk, st.crange);
+    const int64_t maxc = n / st.chunk + n_leaves + 1;
     MKNN_LAUNCH k_chunk_boxes<<<blocks_for(maxc), TPB, 0, s>>>(st.obj, st.crange,
                                                               st.chunk_start + n_leaves, st.box);
   }

@@ -83,7 +83,11 @@ int index_build(DevIndex& ix, const Region& r, const double* x, const double* y,
 // mknn_search.cu).  Objects are 32-byte records (one L2 sector), so the
 // counting-sort scatter writes whole sectors and a candidate's position and
 // id arrive in one sector.
-constexpr int CHUNK = 32;
+// objects per chunk box: 16 for one-slot lists (k <= 32: finer boxes, two
+// chunks per warp step), 32 for k > 32 (buffered admission takes 32
+// candidates per step anyway; coarser best-first order measured faster)
+__host__ __device__ constexpr int chunk_for_k(int k) { return k <= 32 ? 16 : 32; }
+constexpr int MAX_CHUNK = 32;
 
 struct ChunkBox {
   double x_lo, y_lo, x_hi, y_hi;
@@ -128,6 +132,7 @@ struct DevStore {
   int64_t cap_box = 0;
   int32_t* cnt = nullptr;         // n_sub + 2; all zero between ticks
   int32_t* kstart = nullptr;      // n_sub + 2
+  int chunk = 32;                 // objects per chunk (chunk_for_k)
   int32_t* cursor = nullptr;      // bucket counts / cursors of the partition pass
   int32_t* bstart = nullptr;      // bucket starts
   int64_t cap_sub = 0;

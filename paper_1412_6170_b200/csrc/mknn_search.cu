@@ -157,8 +157,9 @@ __device__ __forceinline__ void list_insert(List<KPL>& L, double kd, long long k
 // source index.  trunc(akey(a)) < trunc(akey(b)) implies d2(a) < d2(b), so
 // the result is exactly in canonical (d2, id) order unless two neighbours
 // share a truncated key (a relative gap below 2^-17, or an exact tie such as
-// coincident objects); that case is detected and redone with the exact
-// (d2, id) network.
+// coincident objects); that case -- and, for a merge, equal truncated keys
+// across the cut between the kept and the dropped halves -- is detected and
+// redone with the exact (d2, id) network.
 constexpr uint32_t AKEY_INF = 0x7F800000u;
 
 __device__ __forceinline__ uint32_t akey(double d2, int bits, uint32_t src) {
@@ -204,14 +205,21 @@ __device__ __forceinline__ void batch_sort(double& d, long long& id, int lane) {
 __device__ __forceinline__ void merge_list(List<1>& L, double cd, long long ci, int lane) {
   const uint32_t kl = akey(L.d[0], 6, (uint32_t)lane);
   const uint32_t kc = akey(cd, 6, 32u | (uint32_t)lane);
-  // min(A_i, B_{31-i}) holds the 32 smallest as a bitonic sequence
-  uint32_t m = min(kl, __shfl_sync(FULL, kc, 31 - lane));
+  // min(A_i, B_{31-i}) holds the 32 smallest as a bitonic sequence, max()
+  // the 32 dropped ones
+  const uint32_t rc = __shfl_sync(FULL, kc, 31 - lane);
+  uint32_t m = min(kl, rc);
+  // the largest kept and the smallest dropped key must differ in their
+  // truncated part, or the cut between them is not exact
+  const uint32_t kept_max = __reduce_max_sync(FULL, m);
+  const uint32_t drop_min = __reduce_min_sync(FULL, max(kl, rc));
+  const bool cut_tie = ((kept_max ^ drop_min) >> 6) == 0 && (kept_max >> 6) < (AKEY_INF >> 6);
 #pragma unroll
   for (int j = 16; j > 0; j >>= 1) {
     const uint32_t p = __shfl_xor_sync(FULL, m, j);
     m = (lane & j) ? max(m, p) : min(m, p);
   }
-  if (akey_ties(m, 6, lane)) {
+  if (cut_tie || akey_ties(m, 6, lane)) {
     double c[1] = {cd};
     long long i[1] = {ci};
     bitonic_merge_into<1>(L, c, i, lane);
@@ -337,6 +345,28 @@ __device__ __forceinline__ double mindist2_box(const ChunkBox& b, double qx, dou
   return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
 }
 
+// Pick the 32 / CH nearest candidate boxes of a 32-chunk group (key:
+// approximate distance | lane, ~0 when not a candidate) and map lane groups
+// of CH lanes onto them: this lane's record index cb, valid flag v.
+template <int CH>
+__device__ __forceinline__ void pick_chunks(unsigned key, bool& live, int lane, int ob, int oe,
+                                            int g_rel, int& cb, bool& v) {
+  int mine = -1;
+#pragma unroll
+  for (int p = 0; p < 32 / CH; p++) {
+    const unsigned kmin = __reduce_min_sync(FULL, key);
+    const int src = kmin == 0xffffffffu ? -1 : (int)(kmin & 31u);
+    if (lane == src) {
+      live = false;
+      key = 0xffffffffu;
+    }
+    if (lane / CH == p) mine = src;
+  }
+  const int off = lane % CH;
+  cb = ob + (g_rel + mine) * CH + off;
+  v = mine >= 0 && cb < min(ob + (g_rel + mine + 1) * CH, oe);
+}
+
 // One row of the reference's distance phase (first_iteration's own leaf,
 // engine.py:356-373, or update_nn_lists' assigned leaf, 376-393): every
 // object of the leaf competes for the list.  Chunks whose box min-dist2
@@ -367,11 +397,10 @@ __device__ __forceinline__ void visit_leaf(List<KPL>& L, int k, int leaf, double
       // in the low bits); the visit order only affects speed
       const unsigned key =
           cand ? ((__float_as_uint(__double2float_rd(md)) & ~31u) | (unsigned)lane) : 0xffffffffu;
-      const int src = (int)(__reduce_min_sync(FULL, key) & 31u);
-      if (lane == src) live = false;
-      const int cb = ob + (g - c0 + src) * CHUNK;
-      const bool v = cb + lane < min(cb + CHUNK, oe);
-      const StoreRec r = load_rec(a.obj, cb + lane, v);
+      int cb;
+      bool v;
+      pick_chunks<chunk_for_k(32 * KPL)>(key, live, lane, ob, oe, g - c0, cb, v);
+      const StoreRec r = load_rec(a.obj, cb, v);
       prof_add(a.prof, own ? PROF_OWN_CHUNKS_SCANNED : PROF_EXP_CHUNKS_SCANNED, 1, lane);
       scanned = true;
       if (scan_rec<KPL>(L, kd, ki, v, r, qx, qy, me, lane, a.prof)) {
@@ -467,16 +496,28 @@ __device__ __noinline__ void merge_buffer(List<KPL>& L, const double* bufd, cons
 #pragma unroll
     for (int j = size >> 1; j > 0; j >>= 1) step_key<KPL>(kb, lane, size, j);
   }
-  // min(A_e, B_{N-1-e}): the N smallest as a bitonic sequence
+  // min(A_e, B_{N-1-e}): the N smallest as a bitonic sequence; the largest
+  // kept and the smallest dropped key must differ in their truncated part
+  unsigned long long kept_max = 0, drop_min = ~0ull;
 #pragma unroll
   for (int s = 0; s < KPL; s++) {
     const unsigned long long kl = akey64(L.d[s], SB, (unsigned)((s << 5) | lane));
-    m[s] = min(kl, __shfl_sync(FULL, kb[KPL - 1 - s], 31 - lane));
+    const unsigned long long rb = __shfl_sync(FULL, kb[KPL - 1 - s], 31 - lane);
+    m[s] = min(kl, rb);
+    kept_max = max(kept_max, m[s]);
+    drop_min = min(drop_min, max(kl, rb));
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    kept_max = max(kept_max, __shfl_xor_sync(FULL, kept_max, o));
+    drop_min = min(drop_min, __shfl_xor_sync(FULL, drop_min, o));
+  }
+  const bool cut_tie =
+      ((kept_max ^ drop_min) >> SB) == 0 && (kept_max >> SB) < (AKEY64_INF >> SB);
 #pragma unroll
   for (int j = N >> 1; j > 0; j >>= 1) step_key<KPL>(m, lane, N, j);
   __syncwarp();
-  if (akey64_ties<KPL>(m, SB, lane)) {  // exact (d2, id) networks
+  if (cut_tie || akey64_ties<KPL>(m, SB, lane)) {  // exact (d2, id) networks
     double cd[KPL];
     long long ci[KPL];
 #pragma unroll
@@ -522,11 +563,10 @@ __device__ __forceinline__ void visit_leaf_buf(List<KPL>& L, int k, int leaf, do
       if (!__any_sync(FULL, cand)) break;
       const unsigned key =
           cand ? ((__float_as_uint(__double2float_rd(md)) & ~31u) | (unsigned)lane) : 0xffffffffu;
-      const int src = (int)(__reduce_min_sync(FULL, key) & 31u);
-      if (lane == src) live = false;
-      const int cb = ob + (g - c0 + src) * CHUNK;
-      const bool v = cb + lane < min(cb + CHUNK, oe);
-      const StoreRec r = load_rec(a.obj, cb + lane, v);
+      int cb;
+      bool v;
+      pick_chunks<chunk_for_k(32 * KPL)>(key, live, lane, ob, oe, g - c0, cb, v);
+      const StoreRec r = load_rec(a.obj, cb, v);
       const double d2 = v ? pair_d2(qx, qy, r.x, r.y) : DINF;
       const bool pass = v && d2 <= kd && r.id != me && key_less(d2, r.id, kd, ki);
       const unsigned m = __ballot_sync(FULL, pass);

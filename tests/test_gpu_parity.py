@@ -330,3 +330,24 @@ def test_sliced_host_tick_short_rows():
     with Engine(EngineConfig(k=k, region=Rect.square(10.0), th_quad=4)) as eng:
         res = eng.process_tick(ids, x, y, qi, qx, qy)
     assert_same(res, orc.brute_force_knn(ids, x, y, qi, qx, qy, k))
+
+
+@pytest.mark.parametrize("k,th", [(32, 16), (32, 128), (64, 64), (128, 256)])
+def test_near_ties_at_the_cut(k, th):
+    """A jittered lattice: many candidate distances agree to ~1e-9 relative,
+    so the 32/64-bit key networks see equal truncated keys everywhere --
+    including across the cut between kept and dropped candidates, where the
+    exact (d2, id) network must decide (regression: a missed neighbour
+    0.7 ppm closer than the kept 32nd)."""
+    rng = np.random.default_rng(k + th)
+    g = np.arange(48, dtype=np.float64)
+    gx, gy = np.meshgrid(g, g)
+    x = gx.ravel() + rng.uniform(-1e-7, 1e-7, gx.size) + 1.0
+    y = gy.ravel() + rng.uniform(-1e-7, 1e-7, gy.size) + 1.0
+    n = len(x)
+    ids = rng.permutation(n).astype(np.int64)
+    sel = rng.choice(n, 800, replace=False)
+    qi, qx, qy = ids[sel], x[sel] + rng.uniform(-1e-8, 1e-8, 800), y[sel]
+    with Engine(EngineConfig(k=k, region=Rect.square(50.0), th_quad=th)) as eng:
+        res = eng.process_tick(ids, x, y, qi, qx, qy)
+    assert_same(res, orc.brute_force_knn(ids, x, y, qi, qx, qy, k))
