@@ -930,14 +930,7 @@ int search_launch(const SearchArgs& a, cudaStream_t s) {
   if (a.nq == 0) return 0;
   // k <= 32: 16 queries per warp, 4 warps per CTA, <= 80 registers: the
   // occupancy/latency optimum measured on B200
-  if (a.k <= 32) {
-    static const char* v = getenv("MKNN_B");  // profiling only: batch / warps variants
-    const int b = v ? atoi(v) : 0;
-    if (b == 1) return launch_batched<1, 32, 2, 12>(a, s);
-    if (b == 2) return launch_batched<1, 32, 4, 6>(a, s);
-    if (b == 3) return launch_batched<1, 16, 4, 8>(a, s);
-    return launch_batched<1, 16, 4, 6>(a, s);
-  }
+  if (a.k <= 32) return launch_batched<1, 16, 4, 6>(a, s);
   if (a.k <= 64) return launch_batched<2, 16, 4>(a, s);
   if (a.k <= 128) return launch_batched<4, 8, 4>(a, s);
   if (a.k <= 256) return launch_batched<8, 4, 4>(a, s);
