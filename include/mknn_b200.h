@@ -147,6 +147,16 @@ int mknn_index_export(mknn_engine* h, int32_t* leaf_level, int64_t* leaf_code, i
 /* ObjectStore cell ranges of the last tick (quadindex.py:180-181). */
 int mknn_store_export(mknn_engine* h, int64_t* cell_start, int64_t* cell_end);
 
+/* Result consumer (studies.py:105-108 write_result_block): the CSV lines
+ *   "{tick},{query_id},{rank},{neighbour_id},{distance:.9g}\n"
+ * of a CSR result (qids[nq], offsets[nq + 1], nids / dist[offsets[nq]]),
+ * formatted on `threads` host threads (<= 0: all).  Writes at most cap bytes
+ * to out and returns the byte count, or MKNN_EINVAL if cap is too small.
+ * Host-only: needs no GPU. */
+int64_t mknn_format_result_rows(int64_t tick, int64_t nq, const int64_t* qids,
+                                const int64_t* offsets, const int64_t* nids, const double* dist,
+                                char* out, int64_t cap, int32_t threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -73,6 +73,8 @@ SIGNATURES = {
     "mknn_index_info": (ctypes.c_int, [_vp, _i32p, _i64p, _i64p, _i64p]),
     "mknn_index_export": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mknn_store_export": (ctypes.c_int, [_vp, _vp, _vp]),
+    "mknn_format_result_rows": (ctypes.c_int64, [ctypes.c_int64, ctypes.c_int64, _vp, _vp, _vp, _vp,
+                                                 _vp, ctypes.c_int64, ctypes.c_int32]),
 }
 
 _lib = None
