@@ -351,3 +351,34 @@ def test_near_ties_at_the_cut(k, th):
     with Engine(EngineConfig(k=k, region=Rect.square(50.0), th_quad=th)) as eng:
         res = eng.process_tick(ids, x, y, qi, qx, qy)
     assert_same(res, orc.brute_force_knn(ids, x, y, qi, qx, qy, k))
+
+
+def test_cfg3_full_size_vs_engine_port():
+    """BASELINE.json configs[2] at full size (Gaussian/16, 10M objects, 1M
+    queries, k=32): every row and the per-tick metrics against the pinned C
+    port of the reference engine (OpenMP on the host cores)."""
+    snap = synth.place(10_000_000, "gaussian", seed=3)
+    qi, qx, qy = synth.queries(snap, 1_000_000, seed=3)
+    with Engine(EngineConfig(k=32, region=synth.REGION)) as eng:
+        res = eng.process_tick(snap.ids, snap.x, snap.y, qi, qx, qy)
+        m = eng.last_metrics
+    want = orc.engine_tick(snap.ids, snap.x, snap.y, qi, qx, qy, 32, synth.REGION, 384)
+    assert_same(res, want)
+    assert m.distance_evals == want.metrics["distance_evals"]
+    assert m.pruned_leaves == want.metrics["pruned_leaves"]
+    assert m.active_left == want.metrics["active_left"]
+    assert m.active_right == want.metrics["active_right"]
+
+
+def test_cfg4_full_size_vs_engine_port():
+    """BASELINE.json configs[3] on one GPU (uniform, 100M objects, 10M
+    queries, k=16): every row and the metrics against the C engine port."""
+    snap = synth.place(100_000_000, "uniform", seed=4)
+    qi, qx, qy = synth.queries(snap, 10_000_000, seed=4)
+    with Engine(EngineConfig(k=16, region=synth.REGION)) as eng:
+        res = eng.process_tick(snap.ids, snap.x, snap.y, qi, qx, qy)
+        m = eng.last_metrics
+    want = orc.engine_tick(snap.ids, snap.x, snap.y, qi, qx, qy, 16, synth.REGION, 192)
+    assert_same(res, want)
+    assert m.distance_evals == want.metrics["distance_evals"]
+    assert m.pruned_leaves == want.metrics["pruned_leaves"]
