@@ -128,7 +128,8 @@ __global__ void k_update_claim(const long long* __restrict__ ids, int64_t nu, lo
 __global__ void k_update_apply(const long long* __restrict__ ids, const double* __restrict__ x,
                                const double* __restrict__ y, int64_t nu,
                                const int32_t* __restrict__ slot_of, int32_t* winner,
-                               long long* sids, double* sx, double* sy) {
+                               long long* sids, double* sx, double* sy, int32_t* mark,
+                               int32_t epoch, int32_t* moved, int32_t* n_moved) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nu;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t s = slot_of[i];
@@ -136,6 +137,8 @@ __global__ void k_update_apply(const long long* __restrict__ ids, const double* 
       sids[s] = ids[i];
       sx[s] = x[i];
       sy[s] = y[i];
+      // slots changed since the store was built (once per slot and epoch)
+      if (atomicExch(&mark[s], epoch) != epoch) moved[atomicAdd(n_moved, 1)] = s;
     }
   }
 }
@@ -209,6 +212,13 @@ struct mknn_engine {
   int64_t n_snap = 0;
   long long* hkeys = nullptr; int32_t* hvals = nullptr; int64_t hcap = 0;
   int32_t* winner = nullptr; int64_t cap_winner = 0;
+  // incremental store (delta ticks): slots moved since the store was built
+  int32_t* mark = nullptr;     // per slot: epoch of its last recorded move
+  int32_t* moved = nullptr;    // moved slots
+  int32_t* d_nmoved = nullptr;
+  int64_t h_nmoved = 0;
+  int32_t epoch = 1;
+  unsigned long long* clamped_total = nullptr;  // objects of the store outside the region
   int32_t* slot_of = nullptr; int64_t cap_slot_of = 0;
   int32_t* d_nsnap = nullptr;
   long long* up_ids = nullptr; double *up_x = nullptr, *up_y = nullptr; int64_t cap_up = 0;
@@ -280,21 +290,26 @@ int alloc_store(mknn_engine* h, int64_t n) {
     MKNN_CUDA_OK(cudaMalloc(&h->st.nch, sizeof(int32_t) * (ncap + 2)));
     MKNN_CUDA_OK(cudaMalloc(&h->dq.minmax, sizeof(int64_t) * 2));
     MKNN_CUDA_OK(cudaMalloc(&h->counters, sizeof(unsigned long long) * 8));
+    MKNN_CUDA_OK(cudaMalloc(&h->clamped_total, sizeof(unsigned long long)));
     h->hist_cap = (int)(ncap + 2);
     MKNN_CUDA_OK(cudaMalloc(&h->hist, sizeof(uint32_t) * 2 * h->hist_cap));
   }
   if (n > h->st.cap) {
     int64_t nc = std::max<int64_t>(n, h->st.cap * 3 / 2);
-    cudaFree(h->st.obj);
-    cudaFree(h->st.rec);
-    cudaFree(h->st.key);
-    h->st.rec = nullptr;
-    h->st.obj = nullptr;
-    h->st.key = nullptr;
+    void** old[] = {(void**)&h->st.obj, (void**)&h->st.rec, (void**)&h->st.key,
+                    (void**)&h->st.rmflag, (void**)&h->st.rm_before, (void**)&h->st.mkey};
+    for (auto p : old) {
+      cudaFree(*p);
+      *p = nullptr;
+    }
     h->st.cap = 0;
+    h->st.valid = false;
     MKNN_CUDA_OK(cudaMalloc(&h->st.obj, sizeof(StoreRec) * nc));
     MKNN_CUDA_OK(cudaMalloc(&h->st.rec, sizeof(StoreRec) * nc));
     MKNN_CUDA_OK(cudaMalloc(&h->st.key, sizeof(uint32_t) * nc));
+    MKNN_CUDA_OK(cudaMalloc(&h->st.rmflag, sizeof(int32_t) * (nc + 1)));
+    MKNN_CUDA_OK(cudaMalloc(&h->st.rm_before, sizeof(int32_t) * (nc + 2)));
+    MKNN_CUDA_OK(cudaMalloc(&h->st.mkey, sizeof(uint32_t) * nc));
     h->st.cap = nc;
   }
   return 0;
@@ -383,9 +398,34 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
   h->last_tick_ok = false;
   MKNN_CUDA_OK(cudaEventRecord(h->ev[1], s));
   MKNN_CUDA_OK(cudaMemsetAsync(h->counters, 0, sizeof(unsigned long long) * 8, s));
-  if ((rc = store_index_objects(h->st, h->ix, h->r, ids, x, y, n, h->h_n_leaves, h->h_n_sub,
-                                h->counters + 3, h->scratch.p, s)))
-    return h->set_err(rc);
+  // delta path (the engine's own snapshot): re-index incrementally when the
+  // store still mirrors that snapshot and few slots moved since.  The
+  // incremental pass still moves every surviving record once, so it only
+  // beats the two-pass rebuild below ~5 % moved (measured at 10M objects:
+  // 0.1 % 335 us, 1 % 358 us, 10 % 634 us vs 566 us for a rebuild).
+  const bool from_snap = ids == h->snap_ids && x == h->snap_x && y == h->snap_y;
+  const bool incremental = from_snap && h->st.valid && !rebuild && h->st.n_store <= n &&
+                           (h->h_nmoved + (n - h->st.n_store)) * 20 <= n;
+  if (incremental) {
+    if ((rc = store_update_incremental(h->st, h->ix, h->r, ids, x, y, n, h->moved, h->h_nmoved,
+                                       h->h_n_leaves, h->h_n_sub, h->clamped_total, h->scratch.p,
+                                       s)))
+      return h->set_err(rc);
+    MKNN_CUDA_OK(cudaMemcpyAsync(h->counters + 3, h->clamped_total, sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToDevice, s));
+  } else {
+    if ((rc = store_index_objects(h->st, h->ix, h->r, ids, x, y, n, h->h_n_leaves, h->h_n_sub,
+                                  h->counters + 3, h->scratch.p, s)))
+      return h->set_err(rc);
+    MKNN_CUDA_OK(cudaMemcpyAsync(h->clamped_total, h->counters + 3, sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToDevice, s));
+  }
+  h->st.valid = from_snap;
+  if (from_snap) {  // the store now reflects every recorded move
+    MKNN_CUDA_OK(cudaMemsetAsync(h->d_nmoved, 0, sizeof(int32_t), s));
+    h->h_nmoved = 0;
+    h->epoch++;
+  }
   MKNN_CUDA_OK(cudaEventRecord(h->ev[2], s));
   int bits_used = 0;
   if ((rc = queries_index(h->dq, h->st, h->ix, h->r, qi, qx, qy, nq, h->h_n_sub, h->issuer_bits,
@@ -735,6 +775,15 @@ int snap_reserve(mknn_engine* h, int64_t want) {
   MKNN_CUDA_OK(cudaMalloc(&h->hkeys, sizeof(long long) * hc));
   MKNN_CUDA_OK(cudaMalloc(&h->hvals, sizeof(int32_t) * hc));
   MKNN_CUDA_OK(cudaMalloc(&h->winner, sizeof(int32_t) * nc));
+  cudaFree(h->mark);
+  cudaFree(h->moved);
+  MKNN_CUDA_OK(cudaMalloc(&h->mark, sizeof(int32_t) * nc));
+  MKNN_CUDA_OK(cudaMalloc(&h->moved, sizeof(int32_t) * nc));
+  if (!h->d_nmoved) MKNN_CUDA_OK(cudaMalloc(&h->d_nmoved, sizeof(int32_t)));
+  MKNN_CUDA_OK(cudaMemsetAsync(h->mark, 0, sizeof(int32_t) * nc, s));
+  MKNN_CUDA_OK(cudaMemsetAsync(h->d_nmoved, 0, sizeof(int32_t), s));
+  h->h_nmoved = 0;
+  h->st.valid = false;  // moved-slot history lost
   h->hcap = hc;
   h->cap_winner = nc;
   if (!h->d_nsnap) MKNN_CUDA_OK(cudaMalloc(&h->d_nsnap, sizeof(int32_t)));
@@ -751,6 +800,7 @@ int snap_reserve(mknn_engine* h, int64_t want) {
 int snap_load_dev(mknn_engine* h, int64_t n, const long long* ids, const double* x, const double* y) {
   int rc;
   h->n_snap = 0;
+  h->st.valid = false;
   if ((rc = snap_reserve(h, std::max<int64_t>(n, 1)))) return rc;
   cudaStream_t s = h->stream;
   if (n) {
@@ -779,13 +829,16 @@ int snap_update_dev(mknn_engine* h, int64_t nu, const long long* ids, const doub
   MKNN_LAUNCH k_update_claim<<<gs_blocks(nu), 256, 0, s>>>(ids, nu, h->hkeys, h->hvals, (uint64_t)(h->hcap - 1),
                                                h->d_nsnap, h->winner, h->slot_of);
   MKNN_LAUNCH k_update_apply<<<gs_blocks(nu), 256, 0, s>>>(ids, x, y, nu, h->slot_of, h->winner, h->snap_ids,
-                                               h->snap_x, h->snap_y);
+                                               h->snap_x, h->snap_y, h->mark, h->epoch, h->moved,
+                                               h->d_nmoved);
   MKNN_LAUNCH k_update_reset<<<gs_blocks(nu), 256, 0, s>>>(nu, h->slot_of, h->winner);
   MKNN_CUDA_OK(cudaGetLastError());
-  int32_t nn = 0;
+  int32_t nn = 0, nm = 0;
   MKNN_CUDA_OK(cudaMemcpyAsync(&nn, h->d_nsnap, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  MKNN_CUDA_OK(cudaMemcpyAsync(&nm, h->d_nmoved, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   MKNN_CUDA_OK(cudaStreamSynchronize(s));
   h->n_snap = nn;
+  h->h_nmoved = nm;
   return 0;
 }
 
@@ -850,7 +903,9 @@ void mknn_destroy(mknn_engine* h) {
                   h->out_nids, h->out_dist, h->c_nids, h->c_dist, h->offsets, h->out_qids,
                   h->stats, h->counters, h->hist, h->snap_ids, h->snap_x, h->snap_y, h->hkeys,
                   h->hvals, h->winner, h->slot_of, h->d_nsnap, h->up_ids, h->up_x, h->up_y,
-                  h->tk, h->tk_alt, h->tk_cnt, h->tv, h->tv_alt, h->prof};
+                  h->tk, h->tk_alt, h->tk_cnt, h->tv, h->tv_alt, h->prof, h->mark, h->moved,
+                  h->d_nmoved, h->clamped_total, h->st.kstart_alt, h->st.fill,
+                  h->st.qcnt, h->st.qkstart, h->st.rmflag, h->st.rm_before, h->st.mkey};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   h->scratch.release();

@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(PT_THREADS) k_partition(
       rc[j].x = x[i];
       rc[j].y = y[i];
       rc[j].id = ids[i];
-      rc[j].pad = 0;
+      rc[j].pad = (uint32_t)i;  // input index (the snapshot slot on the delta path)
     }
   }
   __syncthreads();
@@ -299,6 +299,104 @@ __global__ void k_final_scatter(const StoreRec* __restrict__ rec, int64_t n,
     const StoreRec rc = ld_rec(&rec[i]);
     st_rec(&obj[kstart[rc.key] + atomicSub(&cnt[rc.key], 1) - 1], rc);
   }
+}
+
+// ---- incremental store update (delta ticks) -------------------------------
+// The store is a counting sort by sub-cell key; between ticks only the moved
+// snapshot slots change key.  New per-key counts = old counts - removed +
+// added; surviving records keep their order inside their key group, so a
+// record at old position i goes to kstart_new[key] + (i - kstart_old[key])
+// - (removed before i in its group); moved records are appended to their new
+// group after its survivors.  Same multiset per key as a full rebuild, order
+// inside a key group differs -- nothing depends on it (canonical selection).
+__global__ void k_key_counts(const int32_t* __restrict__ kstart, int64_t n_sub,
+                             int32_t* __restrict__ cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_sub;
+       i += (int64_t)gridDim.x * blockDim.x)
+    cnt[i] = kstart[i + 1] - kstart[i];
+}
+
+__device__ __forceinline__ bool outside(double x, double y, const Region& r) {
+  return (x < r.x_lo) | (x > r.x_hi) | (y < r.y_lo) | (y > r.y_hi);  // geometry.py:215-220
+}
+
+// moved slot j: remove its old record (if it had one: found in its old key
+// group, a handful of records, by the slot the record carries), key its new
+// position; slot_key[slot] is every slot's key at the last (re)index
+__global__ void k_moved_keys(const int32_t* __restrict__ moved, int64_t m, int64_t n_old_slots,
+                             uint32_t* __restrict__ slot_key, const int32_t* __restrict__ kold,
+                             const StoreRec* __restrict__ obj, const double* __restrict__ sx,
+                             const double* __restrict__ sy, Region r,
+                             const int32_t* __restrict__ scalars,
+                             const unsigned long long* __restrict__ info,
+                             int32_t* __restrict__ rmflag, int32_t* __restrict__ cnt,
+                             uint32_t* __restrict__ mkey, unsigned long long* clamped) {
+  const int l_deep = scalars[0];
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t sl = moved[j];
+    if (sl < n_old_slots) {
+      const uint32_t ok = slot_key[sl];
+      for (int32_t p = kold[ok], e = kold[ok + 1]; p < e; p++) {
+        if ((int32_t)obj[p].pad == sl) {
+          rmflag[p] = 1;
+          if (outside(obj[p].x, obj[p].y, r)) atomicAdd(clamped, ~0ull);  // -1
+          break;
+        }
+      }
+      atomicSub(&cnt[ok], 1);
+    }
+    const double x = sx[sl], y = sy[sl];
+    uint32_t leaf, key;
+    point_key(x, y, r, l_deep, info, leaf, key);
+    mkey[j] = key;
+    slot_key[sl] = key;
+    atomicAdd(&cnt[key], 1);
+    if (outside(x, y, r)) atomicAdd(clamped, 1ull);
+  }
+}
+
+__global__ void k_move_survivors(const StoreRec* __restrict__ obj, int64_t n_old,
+                                 const int32_t* __restrict__ rmflag,
+                                 const int32_t* __restrict__ rm_before,
+                                 const int32_t* __restrict__ kold, const int32_t* __restrict__ knew,
+                                 StoreRec* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_old;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (rmflag[i]) continue;
+    const StoreRec rc = ld_rec(&obj[i]);
+    const int32_t g = kold[rc.key];
+    st_rec(&out[knew[rc.key] + ((int32_t)i - g) - (rm_before[i] - rm_before[g])], rc);
+  }
+}
+
+__global__ void k_insert_moved(const int32_t* __restrict__ moved, int64_t m,
+                               const uint32_t* __restrict__ mkey, const long long* __restrict__ sids,
+                               const double* __restrict__ sx, const double* __restrict__ sy,
+                               const int32_t* __restrict__ kold, const int32_t* __restrict__ knew,
+                               const int32_t* __restrict__ rm_before, int32_t* __restrict__ fill,
+                               StoreRec* __restrict__ out) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t sl = moved[j];
+    const uint32_t key = mkey[j];
+    const int32_t g0 = kold[key], g1 = kold[key + 1];
+    const int32_t surv = (g1 - g0) - (rm_before[g1] - rm_before[g0]);
+    const int32_t np = knew[key] + surv + atomicAdd(&fill[key], 1);
+    StoreRec rc;
+    rc.x = sx[sl];
+    rc.y = sy[sl];
+    rc.id = sids[sl];
+    rc.key = key;
+    rc.pad = (uint32_t)sl;
+    st_rec(&out[np], rc);
+  }
+}
+
+__global__ void k_fill_reset(const uint32_t* __restrict__ mkey, int64_t m, int32_t* __restrict__ fill) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m;
+       j += (int64_t)gridDim.x * blockDim.x)
+    fill[mkey[j]] = 0;
 }
 
 __global__ void k_q_scatter(int64_t nq, const uint32_t* __restrict__ key,
@@ -498,21 +596,25 @@ int index_build(DevIndex& ix, const Region& r, const double* x, const double* y,
 int store_reserve(DevStore& st, int64_t n_sub, int64_t n_leaves, int64_t n) {
   const int64_t need = std::max<int64_t>(n_sub, 1) + 2;
   if (need > st.cap_sub) {
-    cudaFree(st.cnt);
-    cudaFree(st.kstart);
-    st.cnt = st.kstart = nullptr;
+    int32_t** arrs[] = {&st.cnt, &st.kstart, &st.kstart_alt, &st.fill, &st.qcnt, &st.qkstart};
+    for (auto a : arrs) {
+      cudaFree(*a);
+      *a = nullptr;
+    }
     st.cap_sub = 0;
     const int64_t c = std::max<int64_t>(need, st.cap_sub * 3 / 2);
-    MKNN_CUDA_OK(cudaMalloc(&st.cnt, sizeof(int32_t) * c));
-    MKNN_CUDA_OK(cudaMalloc(&st.kstart, sizeof(int32_t) * c));
+    for (auto a : arrs) MKNN_CUDA_OK(cudaMalloc(a, sizeof(int32_t) * c));
+    MKNN_CUDA_OK(cudaMemset(st.fill, 0, sizeof(int32_t) * c));
+    MKNN_CUDA_OK(cudaMemset(st.qcnt, 0, sizeof(int32_t) * c));
     st.cap_sub = c;
     st.dirty = true;
+    st.valid = false;
   }
-  const int64_t nbox = n / (MAX_CHUNK / 2) + n_leaves + 1;
   if (!st.cursor) {
     MKNN_CUDA_OK(cudaMalloc(&st.cursor, sizeof(int32_t) * (PT_BUCKETS + 1)));
     MKNN_CUDA_OK(cudaMalloc(&st.bstart, sizeof(int32_t) * (PT_BUCKETS + 1)));
   }
+  const int64_t nbox = n / (MAX_CHUNK / 2) + n_leaves + 1;
   if (nbox > st.cap_box) {
     cudaFree(st.box);
     cudaFree(st.crange);
@@ -527,6 +629,27 @@ int store_reserve(DevStore& st, int64_t n_sub, int64_t n_leaves, int64_t n) {
   return 0;
 }
 
+// cell_start, chunk ranges and chunk boxes from st.kstart and st.obj
+static int store_finish(DevStore& st, const DevIndex& ix, int64_t n, int64_t n_leaves,
+                        void* scratch, cudaStream_t s) {
+  MKNN_LAUNCH k_leaf_ranges<<<blocks_for(n_leaves + 1), TPB, 0, s>>>(st.kstart, ix.leaf_sub_base,
+                                                                    n_leaves, st.chunk, st.cell_start,
+                                                                    st.nch);
+  MKNN_CUDA_OK(cudaGetLastError());
+  int rc = exclusive_scan_i32(st.nch, st.chunk_start, n_leaves, scratch, s);
+  if (rc) return rc;
+  if (n > 0) {
+    MKNN_LAUNCH k_chunk_ranges<<<blocks_for(n_leaves), TPB, 0, s>>>(st.cell_start, st.chunk_start,
+                                                                   n_leaves, st.chunk, st.crange);
+    const int64_t maxc = n / st.chunk + n_leaves + 1;
+    MKNN_LAUNCH k_chunk_boxes<<<blocks_for(maxc), TPB, 0, s>>>(st.obj, st.crange,
+                                                              st.chunk_start + n_leaves, st.box);
+  }
+  MKNN_CUDA_OK(cudaGetLastError());
+  st.n_store = n;
+  return 0;
+}
+
 int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const long long* ids,
                         const double* x, const double* y, int64_t n, int64_t n_leaves,
                         int64_t n_sub, unsigned long long* dev_clamped, void* scratch,
@@ -537,7 +660,6 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
   }
   int bshift = 0;
   while ((std::max<int64_t>(n_sub, 1) - 1) >> bshift >= PT_BUCKETS) bshift++;
-  const int nb = (int)(((std::max<int64_t>(n_sub, 1) - 1) >> bshift) + 1);
   MKNN_CUDA_OK(cudaMemsetAsync(st.cursor, 0, sizeof(int32_t) * PT_BUCKETS, s));
   if (n > 0)
     MKNN_LAUNCH k_point_keys<<<grid_stride_blocks(n), TPB, 0, s>>>(
@@ -556,21 +678,40 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
     MKNN_LAUNCH k_final_scatter<<<grid_stride_blocks(n), TPB, 0, s>>>(st.rec, n, st.kstart, st.cnt,
                                                                      st.obj);
   MKNN_CUDA_OK(cudaGetLastError());
-  MKNN_LAUNCH k_leaf_ranges<<<blocks_for(n_leaves + 1), TPB, 0, s>>>(st.kstart, ix.leaf_sub_base,
-                                                                    n_leaves, st.chunk, st.cell_start,
-                                                                    st.nch);
+  return store_finish(st, ix, n, n_leaves, scratch, s);
+}
+
+int store_update_incremental(DevStore& st, const DevIndex& ix, const Region& r,
+                             const long long* sids, const double* sx, const double* sy,
+                             int64_t n_new, const int32_t* moved, int64_t m, int64_t n_leaves,
+                             int64_t n_sub, unsigned long long* dev_clamped_total, void* scratch,
+                             cudaStream_t s) {
+  const int64_t n_old = st.n_store;
+  // cnt <- the current per-key counts, then -removed +added
+  MKNN_LAUNCH k_key_counts<<<grid_stride_blocks(n_sub), TPB, 0, s>>>(st.kstart, n_sub, st.cnt);
+  st.dirty = true;  // cnt no longer all zero
+  MKNN_CUDA_OK(cudaMemsetAsync(st.rmflag, 0, sizeof(int32_t) * (n_old + 1), s));
+  if (m > 0)
+    MKNN_LAUNCH k_moved_keys<<<grid_stride_blocks(m), TPB, 0, s>>>(
+        moved, m, n_old, st.key, st.kstart, st.obj, sx, sy, r, ix.scalars, ix.cell_info, st.rmflag,
+        st.cnt, st.mkey, dev_clamped_total);
   MKNN_CUDA_OK(cudaGetLastError());
-  rc = exclusive_scan_i32(st.nch, st.chunk_start, n_leaves, scratch, s);
+  int rc = exclusive_scan_i32(st.cnt, st.kstart_alt, n_sub, scratch, s);
   if (rc) return rc;
-  if (n > 0) {
-    MKNN_LAUNCH k_chunk_ranges<<<blocks_for(n_leaves), TPB, 0, s>>>(st.cell_start, st.chunk_start,
-                                                                   n_leaves, st.chunk, st.crange);
-    const int64_t maxc = n / st.chunk + n_leaves + 1;
-    MKNN_LAUNCH k_chunk_boxes<<<blocks_for(maxc), TPB, 0, s>>>(st.obj, st.crange,
-                                                              st.chunk_start + n_leaves, st.box);
+  rc = exclusive_scan_i32(st.rmflag, st.rm_before, n_old, scratch, s);
+  if (rc) return rc;
+  if (n_old > 0)
+    MKNN_LAUNCH k_move_survivors<<<grid_stride_blocks(n_old), TPB, 0, s>>>(
+        st.obj, n_old, st.rmflag, st.rm_before, st.kstart, st.kstart_alt, st.rec);
+  if (m > 0) {
+    MKNN_LAUNCH k_insert_moved<<<grid_stride_blocks(m), TPB, 0, s>>>(
+        moved, m, st.mkey, sids, sx, sy, st.kstart, st.kstart_alt, st.rm_before, st.fill, st.rec);
+    MKNN_LAUNCH k_fill_reset<<<grid_stride_blocks(m), TPB, 0, s>>>(st.mkey, m, st.fill);
   }
   MKNN_CUDA_OK(cudaGetLastError());
-  return 0;
+  std::swap(st.obj, st.rec);
+  std::swap(st.kstart, st.kstart_alt);
+  return store_finish(st, ix, n_new, n_leaves, scratch, s);
 }
 
 int issuer_bits(int64_t lo, int64_t hi) {
@@ -585,11 +726,11 @@ int queries_index(DevQueries& dq, DevStore& st, const DevIndex& ix, const Region
   *bits_used = 0;
   if (nq == 0) return 0;
   MKNN_LAUNCH k_point_keys<<<grid_stride_blocks(nq), TPB, 0, s>>>(
-      qx, qy, nq, r, ix.scalars, ix.cell_info, dq.leaf, dq.qkey, st.cnt, nullptr, 0, nullptr);
+      qx, qy, nq, r, ix.scalars, ix.cell_info, dq.leaf, dq.qkey, st.qcnt, nullptr, 0, nullptr);
   MKNN_CUDA_OK(cudaGetLastError());
-  int rc = exclusive_scan_i32(st.cnt, st.kstart, n_sub, scratch, s);
+  int rc = exclusive_scan_i32(st.qcnt, st.qkstart, n_sub, scratch, s);
   if (rc) return rc;
-  MKNN_LAUNCH k_q_scatter<<<grid_stride_blocks(nq), TPB, 0, s>>>(nq, dq.qkey, st.kstart, st.cnt,
+  MKNN_LAUNCH k_q_scatter<<<grid_stride_blocks(nq), TPB, 0, s>>>(nq, dq.qkey, st.qkstart, st.qcnt,
                                                                 dq.order);
   MKNN_CUDA_OK(cudaGetLastError());
 

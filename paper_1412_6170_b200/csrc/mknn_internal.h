@@ -130,8 +130,17 @@ struct DevStore {
   ChunkBox* box = nullptr;        // per chunk
   int2* crange = nullptr;         // per chunk: object range
   int64_t cap_box = 0;
-  int32_t* cnt = nullptr;         // n_sub + 2; all zero between ticks
-  int32_t* kstart = nullptr;      // n_sub + 2
+  int32_t* cnt = nullptr;         // n_sub + 2; all zero between ticks unless dirty
+  int32_t* kstart = nullptr;      // n_sub + 2: first store position of every key
+  int32_t* kstart_alt = nullptr;  // n_sub + 2: incremental update target
+  int32_t* fill = nullptr;        // n_sub + 2: all zero between ticks
+  int32_t* qcnt = nullptr;        // n_sub + 2: query counting sort (all zero between ticks)
+  int32_t* qkstart = nullptr;
+  int32_t* rmflag = nullptr;      // cap + 1: incremental update scratch
+  int32_t* rm_before = nullptr;   // cap + 1
+  uint32_t* mkey = nullptr;       // cap: new keys of the moved slots
+  int64_t n_store = 0;            // records in obj
+  bool valid = false;             // obj/kstart mirror the engine's snapshot (delta path)
   int chunk = 32;                 // objects per chunk (chunk_for_k)
   int32_t* cursor = nullptr;      // bucket counts / cursors of the partition pass
   int32_t* bstart = nullptr;      // bucket starts
@@ -144,10 +153,21 @@ int store_reserve(DevStore& st, int64_t n_sub, int64_t n_leaves, int64_t n);
 
 // quadindex.py:190-213 index_objects; clamped count accumulates into
 // dev_clamped (u64, device).  n_leaves / n_sub are host copies.
+// st.key[i] keeps every input index's key (the snapshot slot's key on the
+// delta path, which store_update_incremental maintains)
 int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const long long* ids,
                         const double* x, const double* y, int64_t n, int64_t n_leaves,
                         int64_t n_sub, unsigned long long* dev_clamped, void* scratch,
                         cudaStream_t s);
+// Delta tick over the snapshot (sids/sx/sy, n_new slots): moved[0, m) are
+// the slots whose position changed (or were appended) since the store was
+// built from that snapshot.  dev_clamped_total: persistent count of objects
+// outside the region.
+int store_update_incremental(DevStore& st, const DevIndex& ix, const Region& r,
+                             const long long* sids, const double* sx, const double* sy,
+                             int64_t n_new, const int32_t* moved, int64_t m, int64_t n_leaves,
+                             int64_t n_sub, unsigned long long* dev_clamped_total, void* scratch,
+                             cudaStream_t s);
 
 // engine.py:201-217 index_queries (leaf ordinal + leaf-grouped order)
 struct DevQueries {

@@ -382,3 +382,53 @@ def test_cfg4_full_size_vs_engine_port():
     assert_same(res, want)
     assert m.distance_evals == want.metrics["distance_evals"]
     assert m.pruned_leaves == want.metrics["pruned_leaves"]
+
+
+@pytest.mark.parametrize("dist", ["uniform", "gaussian"])
+def test_incremental_store_matches_full_rebuild(dist):
+    """Delta ticks re-index incrementally (only the moved slots change key):
+    over many ticks -- repeated updates of an id between queries, updates
+    in several batches, new ids appended, moves out of / back into the
+    region, a query with no update -- every result and metric (incl.
+    clamped_objects) equals a full-snapshot tick on the carried-forward
+    snapshot."""
+    rng = np.random.default_rng(7)
+    n = 40_000
+    snap = synth.place(n, dist, seed=12, hotspots=5, sigma=700.0)
+    ids = list(snap.ids)
+    xs, ys = list(snap.x), list(snap.y)
+    pos = {int(i): j for j, i in enumerate(snap.ids)}
+    with Engine(EngineConfig(k=16, region=synth.REGION)) as full, \
+            Engine(EngineConfig(k=16, region=synth.REGION)) as delta:
+        delta.load(snap.ids, snap.x, snap.y)
+        for t in range(8):
+            for _ in range(int(rng.integers(0, 3))):  # 0-2 update batches before the query
+                u = int(rng.integers(50, 3000))
+                uid = rng.choice(np.asarray(ids), u, replace=True)  # repeats inside a batch
+                ux = rng.uniform(-800, 23300, u)  # some outside the region [0, 22500]
+                uy = rng.uniform(-800, 23300, u)
+                if rng.random() < 0.5:  # brand-new ids
+                    new = np.arange(10 ** 9 + len(ids), 10 ** 9 + len(ids) + 7)
+                    uid = np.concatenate([uid, new])
+                    ux = np.concatenate([ux, rng.uniform(0, 22500, 7)])
+                    uy = np.concatenate([uy, rng.uniform(0, 22500, 7)])
+                delta.update(uid, ux, uy)
+                for i, x, y in zip(uid, ux, uy):  # carry forward, last update wins
+                    i = int(i)
+                    if i not in pos:
+                        pos[i] = len(ids)
+                        ids.append(i)
+                        xs.append(x)
+                        ys.append(y)
+                    else:
+                        xs[pos[i]], ys[pos[i]] = x, y
+            A, X, Y = np.asarray(ids, np.int64), np.asarray(xs), np.asarray(ys)
+            sel = rng.choice(len(A), 2000, replace=False)
+            qi, qx, qy = A[sel], X[sel], Y[sel]
+            a = full.process_tick(A, X, Y, qi, qx, qy)
+            b = delta.query(qi, qx, qy)
+            assert_same(b, a)
+            for key in ("distance_evals", "pruned_leaves", "clamped_objects", "rebuild_flag",
+                        "active_left", "active_right"):
+                assert getattr(delta.last_metrics, key) == getattr(full.last_metrics, key), (t, key)
+        assert delta.snapshot_size == len(ids)
