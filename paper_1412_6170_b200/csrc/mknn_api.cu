@@ -436,7 +436,6 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
   SearchArgs a{};
   a.r = h->r;
   a.k = k;
-  a.l_deep_host = -1;
   a.scalars = h->ix.scalars;
   a.z_map = h->ix.z_map;
   a.leaf_key = h->ix.leaf_key;

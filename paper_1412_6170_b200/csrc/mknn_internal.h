@@ -205,7 +205,6 @@ struct QueryStats {
 struct SearchArgs {
   Region r;
   int k;
-  int l_deep_host;  // -1: read from device scalars
   const int32_t* scalars;
   const int32_t* z_map;
   const uint32_t* leaf_key;
