@@ -84,7 +84,8 @@ int mknn_abi_version(void);
 /* Cumulative number of kernels this library has launched (process-wide). */
 int64_t mknn_kernel_launches(void);
 
-/* Run the engine's work on this cudaStream_t (NULL = the engine's own). */
+/* Run the engine's work on this cudaStream_t (NULL = the engine's own, which is
+ * created non-blocking: pass cudaStreamLegacy, not NULL, for the legacy default stream). */
 int mknn_set_stream(mknn_engine* h, void* cuda_stream);
 
 /* Engine.process_tick (engine.py:601-696) on a full snapshot in HOST memory

@@ -141,6 +141,9 @@ def _tptr(t) -> int:
     return t.data_ptr() if t is not None and t.numel() else 0
 
 
+_CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the legacy NULL stream as a handle
+
+
 class Engine:
     """Stateful tick processor: owns the device index, the rebuild history
     and the device buffers.  Feed it one deduplicated batch per tick."""
@@ -155,6 +158,8 @@ class Engine:
         # count the reference's streamed records T per tick (measurement only)
         self._instrument = False
         self.last_streamed_records = -1
+        self._user_stream = False
+        self._bound_stream = 0
 
     # -- lifecycle (engine.py:570-585) --------------------------------------
     def _handle(self):
@@ -208,9 +213,28 @@ class Engine:
             N.check(N.lib().mknn_set_instrument(self._h, int(self._instrument)), self._h)
 
     def set_stream(self, stream) -> None:
-        """Run on a torch.cuda.Stream (or raw cudaStream_t int)."""
+        """Run on a torch.cuda.Stream (or a raw cudaStream_t int; 0/None =
+        the engine's own stream).  torch's default stream is the legacy NULL
+        stream, passed on as cudaStreamLegacy so the engine stays ordered
+        with it (the engine's own stream is non-blocking)."""
         raw = getattr(stream, "cuda_stream", stream)
+        if hasattr(stream, "cuda_stream") and not raw:
+            raw = _CUDA_STREAM_LEGACY
         N.check(N.lib().mknn_set_stream(self._handle(), ctypes.c_void_p(raw or 0)), self._h)
+        self._user_stream = True
+
+    def _follow_torch_stream(self, t) -> None:
+        """Device-tensor calls run on torch's current stream unless the
+        caller chose a stream: the tensors are produced and consumed there,
+        so the engine's reads and writes stay stream-ordered with them."""
+        if self._user_stream:
+            return
+        import torch
+
+        raw = torch.cuda.current_stream(t.device).cuda_stream or _CUDA_STREAM_LEGACY
+        if raw != self._bound_stream:
+            N.check(N.lib().mknn_set_stream(self._handle(), ctypes.c_void_p(raw)), self._h)
+            self._bound_stream = raw
 
     # -- engine.py:587-589 ---------------------------------------------------
     @property
@@ -324,6 +348,7 @@ class Engine:
         tensors (query_ids, lengths, offsets, neighbour_ids, distances) whose
         CSR arrays are padded to nq*k (first n_results entries valid)."""
         h = self._handle()
+        self._follow_torch_stream(q_issuer)
         nq = int(q_issuer.numel())
         out = out or self.alloc_device_out(nq, q_issuer.device)
         m = N.Metrics()
@@ -362,6 +387,7 @@ class Engine:
         arrays or torch CUDA tensors."""
         h = self._handle()
         if hasattr(ids, "is_cuda") and ids.is_cuda:
+            self._follow_torch_stream(ids)
             N.check(N.lib().mknn_update_device(h, int(ids.numel()), _tptr(ids), _tptr(x), _tptr(y)),
                     h, "mknn_update_device")
             return
@@ -400,6 +426,7 @@ class Engine:
 
     def query_device(self, q_issuer, qx, qy, out=None):
         h = self._handle()
+        self._follow_torch_stream(q_issuer)
         nq = int(q_issuer.numel())
         out = out or self.alloc_device_out(nq, q_issuer.device)
         m = N.Metrics()
