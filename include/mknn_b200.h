@@ -158,6 +158,18 @@ int64_t mknn_format_result_rows(int64_t tick, int64_t nq, const int64_t* qids,
                                 const int64_t* offsets, const int64_t* nids, const double* dist,
                                 char* out, int64_t cap, int32_t threads);
 
+/* Brute-force certificate (audit tooling: oracle.py:41-106
+ * as a tiled fp64 device pass; never on the tick path).  All pointers are
+ * DEVICE memory.  For each query i counts the objects o with
+ * o.id != q_issuer[i] and (d2(q_i, o), o.id) < (kth_d2[i], kth_id[i]) in
+ * canonical order (oracle.py:76-77), d2 with three roundings
+ * (geometry.py:210-212), into out_count[i].  Runs on `stream` (NULL = the
+ * legacy default stream). */
+int mknn_bf_count_device(int64_t n, const int64_t* ids, const double* x, const double* y,
+                         int64_t nq, const int64_t* q_issuer, const double* qx, const double* qy,
+                         const double* kth_d2, const int64_t* kth_id, uint64_t* out_count,
+                         void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -75,6 +75,8 @@ SIGNATURES = {
     "mknn_store_export": (ctypes.c_int, [_vp, _vp, _vp]),
     "mknn_format_result_rows": (ctypes.c_int64, [ctypes.c_int64, ctypes.c_int64, _vp, _vp, _vp, _vp,
                                                  _vp, ctypes.c_int64, ctypes.c_int32]),
+    "mknn_bf_count_device": (ctypes.c_int, [ctypes.c_int64, _vp, _vp, _vp, ctypes.c_int64, _vp, _vp,
+                                            _vp, _vp, _vp, _vp, _vp]),
 }
 
 _lib = None
