@@ -425,12 +425,12 @@ __device__ __forceinline__ void visit_leaf(List<KPL>& L, int k, int leaf, double
 // two neighbours share a truncated key.  A stale k-th key only lets extra
 // candidates into the buffer: the merge keeps the N smallest, so the list
 // is exact.
-template <int KPL, typename KT>
+template <int KPL, typename KT, int S = KPL>  // S: only slots [0, S) take part
 __device__ __forceinline__ void step_key(KT (&kk)[KPL], int lane, int size, int j) {
   if (j >= 32) {
     const int js = j >> 5;
 #pragma unroll
-    for (int s = 0; s < KPL; s++) {
+    for (int s = 0; s < S; s++) {
       if ((s & js) == 0) {
         const int t = s | js;
         const bool asc = ((s << 5) & size) == 0;
@@ -441,7 +441,7 @@ __device__ __forceinline__ void step_key(KT (&kk)[KPL], int lane, int size, int 
     }
   } else {
 #pragma unroll
-    for (int s = 0; s < KPL; s++) {
+    for (int s = 0; s < S; s++) {
       const KT p = __shfl_xor_sync(FULL, kk[s], j);
       const int e = (s << 5) | lane;
       const bool take_min = ((lane & j) == 0) == ((e & size) == 0);
@@ -476,6 +476,26 @@ __device__ __forceinline__ bool akey64_ties(const unsigned long long (&kk)[KPL],
   return __any_sync(FULL, tie);
 }
 
+// bitonic sort of the first S slots (32 * S keys) of kk
+template <int KPL, int S>
+__device__ __forceinline__ void sort_prefix(unsigned long long (&kk)[KPL], int lane) {
+#pragma unroll
+  for (int size = 2; size <= 32 * S; size <<= 1) {
+#pragma unroll
+    for (int j = size >> 1; j > 0; j >>= 1) step_key<KPL, unsigned long long, S>(kk, lane, size, j);
+  }
+}
+
+// a partial flush (nbuf <= 32, one slot) sorts one slot; otherwise all
+// (intermediate widths measured slower: code size)
+template <int KPL>
+__device__ __forceinline__ void sort_used_slots(unsigned long long (&kk)[KPL], int nbuf, int lane) {
+  if (KPL > 1 && KPL <= 4 && nbuf <= 32)
+    sort_prefix<KPL, 1>(kk, lane);
+  else
+    sort_prefix<KPL, KPL>(kk, lane);
+}
+
 // L <- the N smallest of L u buffer[0, nbuf); L ascending.  rowd/rowi: the
 // list's shared-memory home (overwritten), bufd/bufi: the buffer.
 template <int KPL>
@@ -491,11 +511,9 @@ __device__ __noinline__ void merge_buffer(List<KPL>& L, const double* bufd, cons
     rowd[e] = L.d[s];
     rowi[e] = L.id[s];
   }
-#pragma unroll
-  for (int size = 2; size <= N; size <<= 1) {
-#pragma unroll
-    for (int j = size >> 1; j > 0; j >>= 1) step_key<KPL>(kb, lane, size, j);
-  }
+  // sort only the slots that hold candidates: the rest are sentinels that
+  // already sit in ascending order above every real key
+  sort_used_slots<KPL>(kb, nbuf, lane);
   // min(A_e, B_{N-1-e}): the N smallest as a bitonic sequence; the largest
   // kept and the smallest dropped key must differ in their truncated part
   unsigned long long kept_max = 0, drop_min = ~0ull;
@@ -545,11 +563,13 @@ template <int KPL>
 __device__ __forceinline__ void visit_leaf_buf(List<KPL>& L, int k, int leaf, double qx, double qy,
                                                long long me, const SearchArgs& a, int lane,
                                                double* bufd, long long* bufi, double* rowd,
-                                               long long* rowi) {
+                                               long long* rowi, bool own) {
   constexpr int N = 32 * KPL;
   const int ob = __ldg(&a.cell_start[leaf]), oe = __ldg(&a.cell_start[leaf + 1]);
   const int c0 = __ldg(&a.chunk_start[leaf]), c1 = __ldg(&a.chunk_start[leaf + 1]);
   const unsigned lt = (1u << lane) - 1u;
+  prof_add(a.prof, own ? PROF_OWN_CHUNKS_TOTAL : PROF_EXP_CHUNKS_TOTAL, c1 - c0, lane);
+  if (!own) prof_add(a.prof, PROF_EXP_LEAF_VISITS, 1, lane);
   double kd;
   long long ki;
   list_kth<KPL>(L, k, kd, ki);
@@ -567,6 +587,7 @@ __device__ __forceinline__ void visit_leaf_buf(List<KPL>& L, int k, int leaf, do
       bool v;
       pick_chunks<chunk_for_k(32 * KPL)>(key, live, lane, ob, oe, g - c0, cb, v);
       const StoreRec r = load_rec(a.obj, cb, v);
+      prof_add(a.prof, own ? PROF_OWN_CHUNKS_SCANNED : PROF_EXP_CHUNKS_SCANNED, 1, lane);
       const double d2 = v ? pair_d2(qx, qy, r.x, r.y) : DINF;
       const bool pass = v && d2 <= kd && r.id != me && key_less(d2, r.id, kd, ki);
       const unsigned m = __ballot_sync(FULL, pass);
@@ -577,8 +598,10 @@ __device__ __forceinline__ void visit_leaf_buf(List<KPL>& L, int k, int leaf, do
           bufi[pos] = r.id;
         }
         nbuf += __popc(m);
+        prof_add(a.prof, PROF_ADMITTED, __popc(m), lane);
         __syncwarp();
         if (nbuf > N - 32) {
+          prof_add(a.prof, PROF_SORT_MERGES, 1, lane);
           merge_buffer<KPL>(L, bufd, bufi, nbuf, rowd, rowi, lane);
           nbuf = 0;
           list_kth<KPL>(L, k, kd, ki);
@@ -586,7 +609,10 @@ __device__ __forceinline__ void visit_leaf_buf(List<KPL>& L, int k, int leaf, do
       }
     }
   }
-  if (nbuf) merge_buffer<KPL>(L, bufd, bufi, nbuf, rowd, rowi, lane);
+  if (nbuf) {
+    prof_add(a.prof, PROF_INSERTS, 1, lane);  // (k > 32: counts final partial merges)
+    merge_buffer<KPL>(L, bufd, bufi, nbuf, rowd, rowi, lane);
+  }
 }
 
 // engine.py:421-431 coarsest_levels: the coarsest quadrant aligned with the
@@ -749,7 +775,8 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
     if constexpr (KPL == 1)
       visit_leaf<KPL>(L, k, (int)jown, jx, jy, jme, a, lane, true);
     else
-      visit_leaf_buf<KPL>(L, k, (int)jown, jx, jy, jme, a, lane, bufd, bufi, sd + j * N, si + j * N);
+      visit_leaf_buf<KPL>(L, k, (int)jown, jx, jy, jme, a, lane, bufd, bufi, sd + j * N, si + j * N,
+                          true);
     double kd;
     long long ki;
     list_kth<KPL>(L, k, kd, ki);
@@ -794,7 +821,8 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
       if constexpr (KPL == 1)
         visit_leaf<KPL>(L, k, jl, jx, jy, jme, a, lane, false);
       else
-        visit_leaf_buf<KPL>(L, k, jl, jx, jy, jme, a, lane, bufd, bufi, sd + j * N, si + j * N);
+        visit_leaf_buf<KPL>(L, k, jl, jx, jy, jme, a, lane, bufd, bufi, sd + j * N, si + j * N,
+                            false);
       list_store<KPL>(L, sd + j * N, si + j * N, lane);
       double kd;
       long long ki;
@@ -931,10 +959,13 @@ int search_launch(const SearchArgs& a, cudaStream_t s) {
   // k <= 32: 16 queries per warp, 4 warps per CTA, <= 80 registers: the
   // occupancy/latency optimum measured on B200
   if (a.k <= 32) return launch_batched<1, 16, 4, 6>(a, s);
-  if (a.k <= 64) return launch_batched<2, 16, 4>(a, s);
-  if (a.k <= 128) return launch_batched<4, 8, 4>(a, s);
-  if (a.k <= 256) return launch_batched<8, 4, 4>(a, s);
-  if (a.k <= 512) return launch_batched<16, 2, 4>(a, s);
+  // k > 32: the per-warp lists (B * 16 * k bytes of shared memory) bound the
+  // resident warps, so fewer queries per warp win (measured at cfg3 objects:
+  // k = 64 / 128 / 256 / 512 -24 / -18 / -24 / -17 % against 16/8/4/2)
+  if (a.k <= 64) return launch_batched<2, 8, 4>(a, s);
+  if (a.k <= 128) return launch_batched<4, 4, 16>(a, s);
+  if (a.k <= 256) return launch_batched<8, 1, 8>(a, s);
+  if (a.k <= 512) return launch_batched<16, 1, 4>(a, s);
   return fail_msg(E_UNSUPPORTED, "k > 512 is not supported by the device top-k");
 }
 
