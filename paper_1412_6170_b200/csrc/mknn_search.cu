@@ -617,11 +617,28 @@ __device__ __forceinline__ void visit_leaf_buf(List<KPL>& L, int k, int leaf, do
 
 // engine.py:421-431 coarsest_levels: the coarsest quadrant aligned with the
 // cursor (first code for right walks, last code for left walks)
-__device__ __forceinline__ int coarsest_level(long long p, int dir, int l_deep) {
-  const long long a = p + (dir ? 0 : 1);
+__device__ __forceinline__ int coarsest_level(int p, int dir, int l_deep) {
+  const int a = p + (dir ? 0 : 1);  // positions are < 4^l_max = 2^20 (l_max <= 10)
   if (a == 0) return 0;
-  const int tz2 = (__ffsll(a) - 1) >> 1;
+  const int tz2 = (__ffs(a) - 1) >> 1;
   return l_deep - min(tz2, l_deep);
+}
+
+// mindist2_cell (mknn_common.cuh) with the per-level cell width taken from
+// a table: fl(cx * (w * 2^-lvl)) is the same rounding of the same exact
+// product as the reference's fl(ldexp(cx, -lvl) * w) (geometry.py:172-181),
+// since w * 2^-lvl is exact (the kernel checks the widths are 0 or >= 2^-1000)
+__device__ __forceinline__ double mindist2_cell_w(uint32_t code, double wl, double hl,
+                                                  const Region& r, double qx, double qy) {
+  const uint32_t cx = compact_bits32(code), cy = compact_bits32(code >> 1);
+  const double fx = (double)cx, fy = (double)cy;
+  const double xl = __dadd_rn(r.x_lo, __dmul_rn(fx, wl));
+  const double xh = __dadd_rn(r.x_lo, __dmul_rn(__dadd_rn(fx, 1.0), wl));
+  const double yl = __dadd_rn(r.y_lo, __dmul_rn(fy, hl));
+  const double yh = __dadd_rn(r.y_lo, __dmul_rn(__dadd_rn(fy, 1.0), hl));
+  const double dx = dmax(dmax(__dsub_rn(xl, qx), __dsub_rn(qx, xh)), 0.0);
+  const double dy = dmax(dmax(__dsub_rn(yl, qy), __dsub_rn(qy, yh)), 0.0);
+  return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
 }
 
 // instrumentation: record one distance task (dir 0 = own leaf, 1 = left,
@@ -659,32 +676,40 @@ __device__ __noinline__ bool audit_quadrant(const int32_t* __restrict__ z_map,
 // engine.py:396-503 navigate for one query and one direction, run by one
 // lane: returns the assigned leaf ordinal or -1 when the direction is
 // exhausted.  thr is the query's k-th d2 (+inf while the list is not full).
-__device__ __forceinline__ int navigate(const SearchArgs& a, int l_deep, int dir, long long& cursor,
+__device__ __forceinline__ int navigate(const SearchArgs& a, int l_deep, int dir, int& cursor,
                                         double thr, double qx, double qy, long long me,
-                                        uint32_t& prunes, uint32_t& viol) {
-  const long long n_codes = 1LL << (2 * l_deep);
-  const long long sign = dir ? 1 : -1;
-  long long pos = cursor;
+                                        uint32_t& prunes, uint32_t& viol,
+                                        const double2* __restrict__ cw) {
+  const int n_codes = 1 << (2 * l_deep);
+  int pos = cursor;
   if (dir ? pos >= n_codes : pos < 0) return -1;
   const bool full = thr < DINF;  // engine.py:415: thr = MAXDIST iff the list is full
   int lvl = full ? coarsest_level(pos, dir, l_deep) : l_deep;
   for (;;) {
     const int delta = l_deep - lvl;
     const uint32_t qc = (uint32_t)(pos >> (2 * delta));
-    const double md2 = full ? mindist2_cell(lvl, qc, a.r, qx, qy) : 0.0;
+    double md2 = 0.0;
+    if (full) {
+      if (cw) {
+        const double2 wh = cw[lvl];
+        md2 = mindist2_cell_w(qc, wh.x, wh.y, a.r, qx, qy);
+      } else {  // a width below 2^-1000: w * 2^-lvl might not be exact
+        md2 = mindist2_cell(lvl, qc, a.r, qx, qy);
+      }
+    }
     if (md2 > thr) {  // prune (engine.py:447-460; strict, see the header)
       prunes++;
       if (a.audit && audit_quadrant(a.z_map, a.cell_start, a.obj, a.r, l_deep, lvl, qc, thr,
                                     qx, qy, me))
         viol++;
-      pos += sign << (2 * delta);
+      pos += dir ? (1 << (2 * delta)) : -(1 << (2 * delta));
     } else if (lvl < l_deep) {  // descend (engine.py:462-465)
       lvl++;
       continue;
     } else {  // resolve through z_map (engine.py:467-487)
       const int li = __ldg(&a.z_map[pos]);
-      const long long key = __ldg(&a.leaf_key[li]);
-      const long long after = dir ? key + (long long)__ldg(&a.leaf_span[li]) : key - 1;
+      const int key = (int)__ldg(&a.leaf_key[li]);
+      const int after = dir ? key + (int)__ldg(&a.leaf_span[li]) : key - 1;
       if (__ldg(&a.cell_start[li + 1]) > __ldg(&a.cell_start[li])) {
         cursor = after;
         return li;
@@ -734,17 +759,27 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
   double* bufd = reinterpret_cast<double*>(smem_raw) + (size_t)2 * WARPS * B * N + (size_t)w * N;
   long long* bufi = reinterpret_cast<long long*>(smem_raw) + (size_t)2 * WARPS * B * N +
                     (size_t)WARPS * N + (size_t)w * N;
+  const int l_deep = __ldg(&a.scalars[0]);
+  // per-level quadrant widths for navigate (mindist2_cell_w)
+  __shared__ double2 cw_tab[MAX_L_MAX + 1];
+  if (threadIdx.x <= l_deep)
+    cw_tab[threadIdx.x] = make_double2(__dmul_rn(a.r.w, pow2_neg(threadIdx.x)),
+                                       __dmul_rn(a.r.h, pow2_neg(threadIdx.x)));
+  __syncthreads();
+  const bool cw_exact =
+      (a.r.w == 0.0 || a.r.w >= 0x1p-1000) && (a.r.h == 0.0 || a.r.h >= 0x1p-1000);
+  const double2* cw = cw_exact ? cw_tab : nullptr;
   const int64_t t0 = ((int64_t)blockIdx.x * WARPS + w) * B;
   if (t0 >= a.nq) return;
   const int nb = (int)((a.nq - t0) < B ? (a.nq - t0) : B);
-  const int l_deep = __ldg(&a.scalars[0]);
   const int k = a.k;
 
   // per-lane query state (lane q < nb owns query t0 + q)
   const bool mine = lane < nb;
   uint32_t q = 0, own = 0;
   double qx = 0.0, qy = 0.0, thr = DINF;
-  long long me = 0, cur_l = -1, cur_r = 0;
+  long long me = 0;
+  int cur_l = -1, cur_r = 0;
   uint32_t evals = 0, prunes = 0, viol = 0, calls_l = 0, calls_r = 0;
   bool act_l = false, act_r = false;
   if (mine) {
@@ -753,8 +788,8 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
     qy = __ldg(&a.qy[q]);
     me = __ldg(&a.qi[q]);
     own = __ldg(&a.q_leaf[q]);
-    cur_l = (long long)__ldg(&a.leaf_key[own]) - 1;
-    cur_r = (long long)__ldg(&a.leaf_key[own]) + (long long)__ldg(&a.leaf_span[own]);
+    cur_l = (int)__ldg(&a.leaf_key[own]) - 1;
+    cur_r = (int)(__ldg(&a.leaf_key[own]) + __ldg(&a.leaf_span[own]));
     act_l = act_r = true;
     const int pop = __ldg(&a.cell_start[own + 1]) - __ldg(&a.cell_start[own]);
     evals = (uint32_t)pop;  // first_iteration row (rows with 0 candidates dropped, engine.py:334-338)
@@ -792,8 +827,8 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
     const bool act = go_right ? act_r : act_l;
     int li = -1;
     if (act) {
-      long long cur = go_right ? cur_r : cur_l;
-      li = navigate(a, l_deep, go_right ? 1 : 0, cur, thr, qx, qy, me, prunes, viol);
+      int cur = go_right ? cur_r : cur_l;
+      li = navigate(a, l_deep, go_right ? 1 : 0, cur, thr, qx, qy, me, prunes, viol, cw);
       if (go_right) {
         calls_r++;
         cur_r = cur;
