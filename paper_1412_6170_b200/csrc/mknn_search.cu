@@ -724,6 +724,22 @@ __device__ __forceinline__ int navigate(const SearchArgs& a, int l_deep, int dir
   }
 }
 
+// k <= 32 lists kept in the caller's output rows (k slots each, d2 until
+// the emit turns them into distances): no shared memory, so L1 keeps the
+// leaf records and chunk boxes
+__device__ __forceinline__ void row_load(List<1>& L, const double* __restrict__ rd,
+                                         const long long* __restrict__ ri, int k, int lane) {
+  L.d[0] = lane < k ? rd[lane] : DINF;
+  L.id[0] = lane < k ? ri[lane] : IDMAX;
+}
+__device__ __forceinline__ void row_store(const List<1>& L, double* __restrict__ rd,
+                                          long long* __restrict__ ri, int k, int lane) {
+  if (lane < k) {
+    rd[lane] = L.d[0];
+    ri[lane] = L.id[0];
+  }
+}
+
 template <int KPL>
 __device__ __forceinline__ void list_load(List<KPL>& L, const double* __restrict__ sd,
                                           const long long* __restrict__ si, int lane) {
@@ -748,8 +764,9 @@ __device__ __forceinline__ void list_store(const List<KPL>& L, double* __restric
 // lists live in shared memory between steps; leaf scans are warp-wide
 // (32 candidates per ballot), navigation is lane-parallel (lane q walks
 // query q), mirroring the paper's thread-per-query navigation.
-template <int KPL, int B, int WARPS, int MINB>
+template <int KPL, int B, int WARPS, int MINB, bool ROWS = false>
 __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a) {
+  static_assert(!ROWS || KPL == 1, "row-resident lists need k <= 32");
   constexpr int N = 32 * KPL;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -776,7 +793,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
 
   // per-lane query state (lane q < nb owns query t0 + q)
   const bool mine = lane < nb;
-  uint32_t q = 0, own = 0;
+  uint32_t q = 0, own = 0, qrow = 0;
   double qx = 0.0, qy = 0.0, thr = DINF;
   long long me = 0;
   int cur_l = -1, cur_r = 0;
@@ -784,6 +801,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
   bool act_l = false, act_r = false;
   if (mine) {
     q = __ldg(&a.q_order[t0 + lane]);
+    if (ROWS) qrow = __ldg(&a.q_row[q]);
     qx = __ldg(&a.qx[q]);
     qy = __ldg(&a.qy[q]);
     me = __ldg(&a.qi[q]);
@@ -816,7 +834,12 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
     long long ki;
     list_kth<KPL>(L, k, kd, ki);
     if (lane == j) thr = kd;
-    list_store<KPL>(L, sd + j * N, si + j * N, lane);
+    if constexpr (ROWS) {
+      const int64_t o = (int64_t)__shfl_sync(FULL, qrow, j) * k;
+      row_store(L, a.out_dist + o, a.out_nids + o, k, lane);
+    } else {
+      list_store<KPL>(L, sd + j * N, si + j * N, lane);
+    }
   }
   __syncwarp();
 
@@ -852,13 +875,22 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
       const double jx = __shfl_sync(FULL, qx, j), jy = __shfl_sync(FULL, qy, j);
       const long long jme = __shfl_sync(FULL, me, j);
       List<KPL> L;
-      list_load<KPL>(L, sd + j * N, si + j * N, lane);
+      int64_t o = 0;
+      if constexpr (ROWS) {
+        o = (int64_t)__shfl_sync(FULL, qrow, j) * k;
+        row_load(L, a.out_dist + o, a.out_nids + o, k, lane);
+      } else {
+        list_load<KPL>(L, sd + j * N, si + j * N, lane);
+      }
       if constexpr (KPL == 1)
         visit_leaf<KPL>(L, k, jl, jx, jy, jme, a, lane, false);
       else
         visit_leaf_buf<KPL>(L, k, jl, jx, jy, jme, a, lane, bufd, bufi, sd + j * N, si + j * N,
                             false);
-      list_store<KPL>(L, sd + j * N, si + j * N, lane);
+      if constexpr (ROWS)
+        row_store(L, a.out_dist + o, a.out_nids + o, k, lane);
+      else
+        list_store<KPL>(L, sd + j * N, si + j * N, lane);
       double kd;
       long long ki;
       list_kth<KPL>(L, k, kd, ki);
@@ -871,9 +903,12 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
   // _emit: canonical order already; sqrt correctly rounded (engine.py:706)
   for (int j = 0; j < nb; j++) {
     const uint32_t jq = __shfl_sync(FULL, q, j);
-    const uint32_t row = __ldg(&a.q_row[jq]);
+    const uint32_t row = ROWS ? __shfl_sync(FULL, qrow, j) : __ldg(&a.q_row[jq]);
     List<KPL> L;
-    list_load<KPL>(L, sd + j * N, si + j * N, lane);
+    if constexpr (ROWS)
+      row_load(L, a.out_dist + (int64_t)row * k, a.out_nids + (int64_t)row * k, k, lane);
+    else
+      list_load<KPL>(L, sd + j * N, si + j * N, lane);
     int len = 0;
 #pragma unroll
     for (int s = 0; s < KPL; s++) {
@@ -972,28 +1007,29 @@ __global__ void k_rows_compact(const int32_t* __restrict__ len, const long long*
 
 }  // namespace
 
-template <int KPL, int B, int WARPS, int MINB = 1>
+template <int KPL, int B, int WARPS, int MINB = 1, bool ROWS = false>
 int launch_batched(const SearchArgs& a, cudaStream_t s) {
   constexpr int N = 32 * KPL;
-  const size_t smem = (size_t)WARPS * (B + (KPL > 1 ? 1 : 0)) * N * (sizeof(double) + sizeof(long long));
+  const size_t smem = ROWS ? 0 : (size_t)WARPS * (B + (KPL > 1 ? 1 : 0)) * N * (sizeof(double) + sizeof(long long));
   static bool configured = false;
   if (!configured) {
-    MKNN_CUDA_OK(cudaFuncSetAttribute(k_search<KPL, B, WARPS, MINB>,
+    MKNN_CUDA_OK(cudaFuncSetAttribute(k_search<KPL, B, WARPS, MINB, ROWS>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
   const int64_t per_cta = (int64_t)WARPS * B;
   const unsigned blocks = (unsigned)((a.nq + per_cta - 1) / per_cta);
-  MKNN_LAUNCH k_search<KPL, B, WARPS, MINB><<<blocks, 32 * WARPS, smem, s>>>(a);
+  MKNN_LAUNCH k_search<KPL, B, WARPS, MINB, ROWS><<<blocks, 32 * WARPS, smem, s>>>(a);
   MKNN_CUDA_OK(cudaGetLastError());
   return 0;
 }
 
 int search_launch(const SearchArgs& a, cudaStream_t s) {
   if (a.nq == 0) return 0;
-  // k <= 32: 16 queries per warp, 4 warps per CTA, <= 80 registers: the
-  // occupancy/latency optimum measured on B200
-  if (a.k <= 32) return launch_batched<1, 16, 4, 6>(a, s);
+  // k <= 32: lists in the output rows (no shared memory: L1 holds the leaf
+  // records and boxes), 32 queries per warp (every lane navigates), 2 warps
+  // per CTA, <= 72 registers: the optimum measured on B200
+  if (a.k <= 32) return launch_batched<1, 32, 2, 14, true>(a, s);
   // k > 32: the per-warp lists (B * 16 * k bytes of shared memory) bound the
   // resident warps, so fewer queries per warp win (measured at cfg3 objects:
   // k = 64 / 128 / 256 / 512 -24 / -18 / -24 / -17 % against 16/8/4/2)
