@@ -727,16 +727,42 @@ __device__ __forceinline__ int navigate(const SearchArgs& a, int l_deep, int dir
 // k <= 32 lists kept in the caller's output rows (k slots each, d2 until
 // the emit turns them into distances): no shared memory, so L1 keeps the
 // leaf records and chunk boxes
+__device__ __forceinline__ unsigned long long l2_evict_last() {
+  unsigned long long p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ long long ld_keep(const long long* p, unsigned long long pol) {
+  long long v;
+  asm volatile("ld.global.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_keep(const double* p, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_keep(long long* p, long long v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_keep(double* p, double v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
+// the rows are re-read by the warp's later visits: keep them in L2
+// (evict_last) while the streamed object records come and go
 __device__ __forceinline__ void row_load(List<1>& L, const double* __restrict__ rd,
                                          const long long* __restrict__ ri, int k, int lane) {
-  L.d[0] = lane < k ? rd[lane] : DINF;
-  L.id[0] = lane < k ? ri[lane] : IDMAX;
+  const unsigned long long pol = l2_evict_last();
+  L.d[0] = lane < k ? ld_keep(rd + lane, pol) : DINF;
+  L.id[0] = lane < k ? ld_keep(ri + lane, pol) : IDMAX;
 }
 __device__ __forceinline__ void row_store(const List<1>& L, double* __restrict__ rd,
                                           long long* __restrict__ ri, int k, int lane) {
+  const unsigned long long pol = l2_evict_last();
   if (lane < k) {
-    rd[lane] = L.d[0];
-    ri[lane] = L.id[0];
+    st_keep(rd + lane, L.d[0], pol);
+    st_keep(ri + lane, L.id[0], pol);
   }
 }
 
@@ -915,9 +941,9 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
       const int e = (s << 5) | lane;
       const bool ok = e < k && L.d[s] < DINF;
       len += __popc(__ballot_sync(FULL, ok));
-      if (ok) {
-        a.out_nids[(int64_t)row * k + e] = L.id[s];
-        a.out_dist[(int64_t)row * k + e] = __dsqrt_rn(L.d[s]);
+      if (ok) {  // final values: streaming stores
+        __stcs(&a.out_nids[(int64_t)row * k + e], L.id[s]);
+        __stcs(&a.out_dist[(int64_t)row * k + e], __dsqrt_rn(L.d[s]));
       }
     }
     if (lane == 0) a.out_len[row] = len;
@@ -1027,9 +1053,10 @@ int launch_batched(const SearchArgs& a, cudaStream_t s) {
 int search_launch(const SearchArgs& a, cudaStream_t s) {
   if (a.nq == 0) return 0;
   // k <= 32: lists in the output rows (no shared memory: L1 holds the leaf
-  // records and boxes), 32 queries per warp (every lane navigates), 2 warps
-  // per CTA, <= 72 registers: the optimum measured on B200
-  if (a.k <= 32) return launch_batched<1, 32, 2, 14, true>(a, s);
+  // records and boxes), 32 queries per warp (every lane navigates), one
+  // warp per CTA (a finished warp frees its slot at once), <= 64 registers:
+  // the optimum measured on B200
+  if (a.k <= 32) return launch_batched<1, 32, 1, 32, true>(a, s);
   // k > 32: the per-warp lists (B * 16 * k bytes of shared memory) bound the
   // resident warps, so fewer queries per warp win (measured at cfg3 objects:
   // k = 64 / 128 / 256 / 512 -24 / -18 / -24 / -17 % against 16/8/4/2)
