@@ -332,7 +332,8 @@ def main() -> int:
         h_out = (torch.empty(nq, dtype=torch.int64).pin_memory().numpy(),
                  torch.empty(nq, dtype=torch.int32).pin_memory().numpy(),
                  torch.empty(nq * k, dtype=torch.int64).pin_memory().numpy(),
-                 torch.empty(nq * k, dtype=torch.float64).pin_memory().numpy())
+                 torch.empty(nq * k, dtype=torch.float64).pin_memory().numpy(),
+                 np.empty(nq + 1, dtype=np.int64))
         if delta:
             h_up = [[pin(a[ulo:uhi]) for a in b] for b in batches]
             if world == 1:

@@ -180,6 +180,8 @@ struct mknn_engine {
   int issuer_bits = -1;        // issuer-id bits of the last tick (plans the row sort)
   cudaStream_t copy_stream = nullptr;  // result slices device -> host
   cudaEvent_t slice_ev[N_SLICES] = {};
+  cudaEvent_t q_ready = nullptr;  // host query batch staged on copy_stream
+  bool q_pending = false;
   bool rows_in_host = false;   // the sliced host tick already delivered qids/len/rows
   bool retry_rebuild = false;  // false: the store's sub-cell counters may be dirty
   int32_t h_l_deep = 0;
@@ -428,6 +430,10 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
   }
   MKNN_CUDA_OK(cudaEventRecord(h->ev[2], s));
   int bits_used = 0;
+  if (h->q_pending) {  // host queries staged on the copy stream (stage_queries)
+    MKNN_CUDA_OK(cudaStreamWaitEvent(s, h->q_ready, 0));
+    h->q_pending = false;
+  }
   if ((rc = queries_index(h->dq, h->st, h->ix, h->r, qi, qx, qy, nq, h->h_n_sub, h->issuer_bits,
                           &bits_used, o.qids, h->scratch.p, s)))
     return h->set_err(rc);
@@ -734,12 +740,18 @@ int stage_queries(mknn_engine* h, int64_t nq, const int64_t* qi, const double* q
   c = h->cap_qin;
   if ((rc = grow(h->in_qy, c, std::max<int64_t>(nq, 1)))) return rc;
   h->cap_qin = c;
-  cudaStream_t s = h->stream;
+  // on the copy stream: the queries cross PCIe while the objects are
+  // (re-)indexed; the tick waits for them just before index_queries
+  cudaStream_t cs = h->copy_stream;
+  MKNN_CUDA_OK(cudaEventRecord(h->ev[7], h->stream));  // inputs of the previous call consumed
+  MKNN_CUDA_OK(cudaStreamWaitEvent(cs, h->ev[7], 0));
   if (nq) {
-    MKNN_CUDA_OK(cudaMemcpyAsync(h->in_qi, qi, sizeof(int64_t) * nq, cudaMemcpyHostToDevice, s));
-    MKNN_CUDA_OK(cudaMemcpyAsync(h->in_qx, qx, sizeof(double) * nq, cudaMemcpyHostToDevice, s));
-    MKNN_CUDA_OK(cudaMemcpyAsync(h->in_qy, qy, sizeof(double) * nq, cudaMemcpyHostToDevice, s));
+    MKNN_CUDA_OK(cudaMemcpyAsync(h->in_qi, qi, sizeof(int64_t) * nq, cudaMemcpyHostToDevice, cs));
+    MKNN_CUDA_OK(cudaMemcpyAsync(h->in_qx, qx, sizeof(double) * nq, cudaMemcpyHostToDevice, cs));
+    MKNN_CUDA_OK(cudaMemcpyAsync(h->in_qy, qy, sizeof(double) * nq, cudaMemcpyHostToDevice, cs));
   }
+  MKNN_CUDA_OK(cudaEventRecord(h->q_ready, cs));
+  h->q_pending = true;
   return 0;
 }
 
@@ -879,6 +891,8 @@ int mknn_create(const mknn_config* cfg, mknn_engine** out) {
     if (cudaEventCreate(&h->ev[i]) != cudaSuccess) rc = E_CUDA;
   for (int i = 0; i < N_SLICES && !rc; i++)
     if (cudaEventCreateWithFlags(&h->slice_ev[i], cudaEventDisableTiming) != cudaSuccess) rc = E_CUDA;
+  if (!rc && cudaEventCreateWithFlags(&h->q_ready, cudaEventDisableTiming) != cudaSuccess)
+    rc = E_CUDA;
   if (!rc && cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
     rc = E_CUDA;
   if (rc) {
@@ -913,6 +927,7 @@ void mknn_destroy(mknn_engine* h) {
     if (e) cudaEventDestroy(e);
   for (auto& e : h->slice_ev)
     if (e) cudaEventDestroy(e);
+  if (h->q_ready) cudaEventDestroy(h->q_ready);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;

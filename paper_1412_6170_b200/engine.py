@@ -160,6 +160,7 @@ class Engine:
         self.last_streamed_records = -1
         self._user_stream = False
         self._bound_stream = 0
+        self._ramp = np.zeros(0, np.int64)  # 0..nq, reused for full-row CSR offsets
 
     # -- lifecycle (engine.py:570-585) --------------------------------------
     def _handle(self):
@@ -300,19 +301,25 @@ class Engine:
         self.last_metrics = tm
         return tm
 
-    def _result(self, qids, lens, nids, dist, n_results) -> TickResult:
+    def _result(self, qids, lens, nids, dist, n_results, offsets=None) -> TickResult:
         k = self.config.k
-        if n_results == len(lens) * k:  # every row full: the CSR is the padded rows
-            offsets = np.arange(0, (len(lens) + 1) * k, k, dtype=np.int64)
+        nq = len(lens)
+        if offsets is None:
+            offsets = np.empty(nq + 1, np.int64)
+        if n_results == nq * k:  # every row full: the CSR is the padded rows
+            if len(self._ramp) != nq + 1:
+                self._ramp = np.arange(nq + 1, dtype=np.int64)
+            np.multiply(self._ramp, k, out=offsets)
         else:
-            offsets = np.zeros(len(lens) + 1, np.int64)
+            offsets[0] = 0
             np.cumsum(lens, out=offsets[1:])
         return TickResult(query_ids=qids, lengths=lens, offsets=offsets,
                           neighbour_ids=nids[:n_results], distances=dist[:n_results])
 
     def process_tick(self, ids, x, y, q_issuer, qx, qy, out=None) -> TickResult:
         """engine.py:601-696.  ``out`` optionally supplies (qids, lens, nids,
-        dist) host buffers (e.g. pinned) of sizes nq, nq, nq*k, nq*k."""
+        dist[, offsets]) host buffers (e.g. pinned) of sizes nq, nq, nq*k, nq*k
+        [, nq+1]; the returned TickResult views them."""
         h = self._handle()
         k = self.config.k
         ids = np.ascontiguousarray(ids, dtype=np.int64)
@@ -330,13 +337,14 @@ class Engine:
             nids = np.empty(nq * k, np.int64)
             dist = np.empty(nq * k, np.float64)
         else:
-            qids, lens, nids, dist = out
+            qids, lens, nids, dist = out[:4]
         m = N.Metrics()
         N.check(N.lib().mknn_tick(h, n, _ptr(ids), _ptr(x), _ptr(y), nq, _ptr(q_issuer), _ptr(qx),
                                   _ptr(qy), _ptr(qids), _ptr(lens), _ptr(nids), _ptr(dist),
                                   ctypes.byref(m)), h, "mknn_tick")
         self._finish(m)
-        return self._result(qids, lens, nids, dist, m.n_results)
+        offs = out[4] if out is not None and len(out) > 4 else None
+        return self._result(qids, lens, nids, dist, m.n_results, offs)
 
     def process_batch(self, batch) -> TickResult:
         """engine.py:698-701."""
@@ -416,13 +424,14 @@ class Engine:
             nids = np.empty(nq * k, np.int64)
             dist = np.empty(nq * k, np.float64)
         else:
-            qids, lens, nids, dist = out
+            qids, lens, nids, dist = out[:4]
         m = N.Metrics()
         N.check(N.lib().mknn_query(h, nq, _ptr(q_issuer), _ptr(qx), _ptr(qy), _ptr(qids),
                                    _ptr(lens), _ptr(nids), _ptr(dist), ctypes.byref(m)), h,
                 "mknn_query")
         self._finish(m)
-        return self._result(qids, lens, nids, dist, m.n_results)
+        offs = out[4] if out is not None and len(out) > 4 else None
+        return self._result(qids, lens, nids, dist, m.n_results, offs)
 
     def query_device(self, q_issuer, qx, qy, out=None):
         h = self._handle()

@@ -286,10 +286,16 @@ def test_pinned_host_outputs_written_in_place(n, k):
     pin = lambda shape, dt: torch.empty(shape, dtype=dt).pin_memory().numpy()  # noqa: E731
     out = (pin(nq, torch.int64), pin(nq, torch.int32), pin(nq * k, torch.int64),
            pin(nq * k, torch.float64))
+    offs = np.full(nq + 1, -7, np.int64)
+    want = orc.brute_force_knn(ids, x, y, qi, qx, qy, k)
     with Engine(EngineConfig(k=k, region=Rect.square(100.0), th_quad=24)) as eng:
         for _ in range(2):
             res = eng.process_tick(ids, x, y, qi, qx, qy, out=out)
-            assert_same(res, orc.brute_force_knn(ids, x, y, qi, qx, qy, k))
+            assert_same(res, want)
+            # optional caller-owned offsets buffer: filled in place
+            res = eng.process_tick(ids, x, y, qi, qx, qy, out=out + (offs,))
+            assert_same(res, want)
+            assert res.offsets is offs and np.array_equal(offs, want.offsets)
 
 
 def test_sliced_host_tick_equals_device_tick():
