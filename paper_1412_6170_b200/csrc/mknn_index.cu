@@ -294,10 +294,20 @@ __global__ void __launch_bounds__(PT_THREADS) k_partition(
 __global__ void k_final_scatter(const StoreRec* __restrict__ rec, int64_t n,
                                 const int32_t* __restrict__ kstart, int32_t* __restrict__ cnt,
                                 StoreRec* __restrict__ obj) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const StoreRec rc = ld_rec(&rec[i]);
-    st_rec(&obj[kstart[rc.key] + atomicSub(&cnt[rc.key], 1) - 1], rc);
+  constexpr int U = 4;  // records in flight per thread (the atomics are latency-bound)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+    StoreRec rc[U];
+    int pos[U];
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (i0 + u * stride < n) rc[u] = ld_rec(&rec[i0 + u * stride]);
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (i0 + u * stride < n) pos[u] = kstart[rc[u].key] + atomicSub(&cnt[rc[u].key], 1) - 1;
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (i0 + u * stride < n) st_rec(&obj[pos[u]], rc[u]);
   }
 }
 
