@@ -460,6 +460,7 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
   a.out_len = o.len;
   a.out_nids = o.nids;  // padded rows in the output itself (rows_compact)
   a.out_dist = o.dist;
+  a.n_objects = n;
   a.stats = h->stats;
   a.audit = h->cfg.audit_pruning;
   {
@@ -520,7 +521,6 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
       aj.q_order = sorder + r0;
       aj.nq = r1 - r0;
       aj.stats = h->stats + r0;
-      aj.density_div = N_SLICES;  // 1/N_SLICES of the queries per leaf
       if ((rc = search_launch(aj, s))) return h->set_err(rc);
       MKNN_CUDA_OK(cudaEventRecord(h->slice_ev[j], s));
       MKNN_CUDA_OK(cudaStreamWaitEvent(h->copy_stream, h->slice_ev[j], 0));

@@ -226,7 +226,7 @@ struct SearchArgs {
   QueryStats* stats;      // [nq] by leaf-grouped position
   int audit;
   int debug_phase; // profiling only: 1 = own leaf only (results invalid)
-  int density_div;  // the batch holds 1/density_div of the tick's queries (row slices)
+  int64_t n_objects;  // objects of the tick (the query density picks the warp batch)
   // profiling only (MKNN_PROF=1): work counters, see PROF_* in mknn_search.cu
   unsigned long long* prof;
   // instrumentation: (dir, iteration, leaf) keys of every distance task

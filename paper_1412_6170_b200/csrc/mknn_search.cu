@@ -1056,11 +1056,15 @@ int search_launch(const SearchArgs& a, cudaStream_t s) {
   // records and boxes), 32 queries per warp (every lane navigates), one
   // warp per CTA (a finished warp frees its slot at once), <= 64 registers:
   // the optimum measured on B200
-  // A row slice holds a fraction of every leaf's queries (mknn_api.cu
-  // host ticks): fewer queries per warp keep a warp's queries on as few
-  // leaves as in a whole tick (measured: 4 slices, 8 per warp -0.9 ms e2e).
-  if (a.k <= 32 && a.density_div >= 4) return launch_batched<1, 8, 1, 32, true>(a, s);
-  if (a.k <= 32 && a.density_div >= 2) return launch_batched<1, 16, 1, 32, true>(a, s);
+  // Queries per warp follow the query density (queries per object): a
+  // sparser batch spreads a warp's queries over more leaves and its
+  // own-leaf scans stop sharing L1 lines (measured at 10M objects: 1M
+  // queries -> 32; 300K -> 8: 1.75 -> 1.01 ms; a 1/4 row slice of a host
+  // tick -> 8)
+  const double qd = (double)a.nq / (double)(a.n_objects > 0 ? a.n_objects : 1);
+  if (a.k <= 32 && qd < 0.015) return launch_batched<1, 4, 1, 32, true>(a, s);
+  if (a.k <= 32 && qd < 0.04) return launch_batched<1, 8, 1, 32, true>(a, s);
+  if (a.k <= 32 && qd < 0.06) return launch_batched<1, 16, 1, 32, true>(a, s);
   if (a.k <= 32) return launch_batched<1, 32, 1, 32, true>(a, s);
   // k > 32: the per-warp lists (B * 16 * k bytes of shared memory) bound the
   // resident warps, so fewer queries per warp win (measured at cfg3 objects:
