@@ -166,6 +166,15 @@ int64_t us_between(cudaEvent_t a, cudaEvent_t b) {
 constexpr int N_SLICES = 4;
 constexpr int64_t SLICE_MIN_QUERIES = 65536;
 
+// pinned landing block of a tick's small device->host readbacks
+struct PinBlock {
+  static constexpr int HIST = 256;
+  unsigned long long cnt[8];
+  int64_t mm[2];
+  int64_t total;
+  uint32_t hist[2][HIST];
+};
+
 struct mknn_engine {
   mknn_config cfg{};
   Region r{};
@@ -181,6 +190,7 @@ struct mknn_engine {
   cudaStream_t copy_stream = nullptr;  // result slices device -> host
   cudaEvent_t slice_ev[N_SLICES] = {};
   cudaEvent_t q_ready = nullptr;  // host query batch staged on copy_stream
+  PinBlock* pin = nullptr;
   bool q_pending = false;
   bool rows_in_host = false;   // the sliced host tick already delivered qids/len/rows
   bool retry_rebuild = false;  // false: the store's sub-cell counters may be dirty
@@ -559,13 +569,22 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
     return h->set_err(rc);
   MKNN_CUDA_OK(cudaEventRecord(h->ev[5], s));
 
-  unsigned long long cnt[8];
-  MKNN_CUDA_OK(cudaMemcpyAsync(cnt, h->counters, sizeof(cnt), cudaMemcpyDeviceToHost, s));
-  int64_t mm[2] = {0, 0};
-  if (nq) MKNN_CUDA_OK(cudaMemcpyAsync(mm, h->dq.minmax, sizeof(mm), cudaMemcpyDeviceToHost, s));
-  int64_t total = 0;
-  MKNN_CUDA_OK(cudaMemcpyAsync(&total, o.offsets + nq, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  // every small readback of the tick in one pinned block, one sync
+  if (!h->pin) MKNN_CUDA_OK(cudaMallocHost(&h->pin, sizeof(PinBlock)));
+  PinBlock& pb = *h->pin;
+  MKNN_CUDA_OK(cudaMemcpyAsync(pb.cnt, h->counters, sizeof(pb.cnt), cudaMemcpyDeviceToHost, s));
+  pb.mm[0] = pb.mm[1] = 0;
+  if (nq) MKNN_CUDA_OK(cudaMemcpyAsync(pb.mm, h->dq.minmax, sizeof(pb.mm), cudaMemcpyDeviceToHost, s));
+  MKNN_CUDA_OK(cudaMemcpyAsync(&pb.total, o.offsets + nq, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  const int64_t hpre = std::min<int64_t>(h->hist_cap, PinBlock::HIST);
+  if (nq)
+    for (int d = 0; d < 2; d++)
+      MKNN_CUDA_OK(cudaMemcpyAsync(pb.hist[d], h->hist + (int64_t)d * h->hist_cap,
+                                   sizeof(uint32_t) * hpre, cudaMemcpyDeviceToHost, s));
   MKNN_CUDA_OK(cudaStreamSynchronize(s));
+  const unsigned long long* cnt = pb.cnt;
+  const int64_t* mm = pb.mm;
+  const int64_t total = pb.total;
   if (sliced) {
     MKNN_CUDA_OK(cudaStreamSynchronize(h->copy_stream));
     h->rows_in_host = total == nq * (int64_t)k;  // short rows: the caller copies the CSR
@@ -586,17 +605,18 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
   for (int d = 0; d < 2; d++) {
     h->active[d].clear();
     if (nq == 0) continue;
-    // fetch the histogram prefix that can be non-zero
-    std::vector<uint32_t> hh;
-    int64_t lim = std::min<int64_t>(h->hist_cap, 4096);
+    // the histogram prefix that can be non-zero (read with the counters;
+    // longer walks fetch more)
+    std::vector<uint32_t> hh(pb.hist[d], pb.hist[d] + hpre);
+    int64_t lim = hpre;
     for (;;) {
-      hh.resize(lim);
-      MKNN_CUDA_OK(cudaMemcpy(hh.data(), h->hist + (int64_t)d * h->hist_cap, sizeof(uint32_t) * lim,
-                              cudaMemcpyDeviceToHost));
       int64_t seen = 0;
       for (auto v : hh) seen += v;
       if (seen >= nq || lim >= h->hist_cap) break;
       lim = std::min<int64_t>(h->hist_cap, lim * 16);
+      hh.resize(lim);
+      MKNN_CUDA_OK(cudaMemcpy(hh.data(), h->hist + (int64_t)d * h->hist_cap, sizeof(uint32_t) * lim,
+                              cudaMemcpyDeviceToHost));
     }
     int64_t maxc = 0;
     for (int64_t c = 0; c < (int64_t)hh.size(); c++)
@@ -928,6 +948,7 @@ void mknn_destroy(mknn_engine* h) {
   for (auto& e : h->slice_ev)
     if (e) cudaEventDestroy(e);
   if (h->q_ready) cudaEventDestroy(h->q_ready);
+  if (h->pin) cudaFreeHost(h->pin);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
