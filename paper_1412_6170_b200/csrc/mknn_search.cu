@@ -961,6 +961,15 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
 
 constexpr int HIST_SMEM = 1024;
 
+// one histogram count; lanes holding the same value (most queries make the
+// same few navigate calls) are combined into one atomic by their leader
+__device__ __forceinline__ void hist_add(uint32_t* sh, uint32_t* gl, int cap, uint32_t v) {
+  const unsigned peers = __match_any_sync(__activemask(), v);
+  if ((int)(threadIdx.x & 31) != __ffs(peers) - 1) return;
+  if (v < HIST_SMEM) atomicAdd(&sh[v], (uint32_t)__popc(peers));
+  else if ((int64_t)v < cap) atomicAdd(&gl[v], (uint32_t)__popc(peers));
+}
+
 __global__ void k_stats_reduce(const QueryStats* __restrict__ st, int64_t nq,
                                unsigned long long* tot, uint32_t* hist_l, uint32_t* hist_r,
                                int hist_cap) {
@@ -974,10 +983,8 @@ __global__ void k_stats_reduce(const QueryStats* __restrict__ st, int64_t nq,
     ev += s.evals;
     pr += s.prunes;
     vi += s.violations;
-    if (s.nav_left < HIST_SMEM) atomicAdd(&hl[s.nav_left], 1u);
-    else if (s.nav_left < hist_cap) atomicAdd(&hist_l[s.nav_left], 1u);
-    if (s.nav_right < HIST_SMEM) atomicAdd(&hr[s.nav_right], 1u);
-    else if (s.nav_right < hist_cap) atomicAdd(&hist_r[s.nav_right], 1u);
+    hist_add(hl, hist_l, hist_cap, s.nav_left);
+    hist_add(hr, hist_r, hist_cap, s.nav_right);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
