@@ -375,7 +375,8 @@ __device__ __forceinline__ void pick_chunks(unsigned key, bool& live, int lane, 
 // are visited nearest box first, so the list tightens early.
 template <int KPL>
 __device__ __forceinline__ void visit_leaf(List<KPL>& L, int k, int leaf, double qx, double qy,
-                                           long long me, const SearchArgs& a, int lane, bool own) {
+                                           long long me, const SearchArgs& a, int lane, bool own,
+                                           double cap = DINF) {
   const int ob = __ldg(&a.cell_start[leaf]), oe = __ldg(&a.cell_start[leaf + 1]);
   const int c0 = __ldg(&a.chunk_start[leaf]), c1 = __ldg(&a.chunk_start[leaf + 1]);
   prof_add(a.prof, own ? PROF_OWN_CHUNKS_TOTAL : PROF_EXP_CHUNKS_TOTAL, c1 - c0, lane);
@@ -383,9 +384,16 @@ __device__ __forceinline__ void visit_leaf(List<KPL>& L, int k, int leaf, double
   bool scanned = false, admitted = false;  // profiling only
   (void)scanned;
   (void)admitted;
+  // cap: an upper bound of the k-th d2 of this leaf's objects (see
+  // k_search); the effective admission key is the smaller of (k-th d2, k-th
+  // id) and (cap, IDMAX), so every admitted candidate also has d2 <= cap
   double kd;
   long long ki;
   list_kth<KPL>(L, k, kd, ki);
+  if (cap < kd) {
+    kd = cap;
+    ki = IDMAX;
+  }
   for (int g = c0; g < c1; g += 32) {
     bool live = g + lane < c1;
     double md = DINF;
@@ -405,6 +413,10 @@ __device__ __forceinline__ void visit_leaf(List<KPL>& L, int k, int leaf, double
       scanned = true;
       if (scan_rec<KPL>(L, kd, ki, v, r, qx, qy, me, lane, a.prof)) {
         list_kth<KPL>(L, k, kd, ki);
+        if (cap < kd) {
+          kd = cap;
+          ki = IDMAX;
+        }
         admitted = true;
       }
     }
@@ -840,11 +852,28 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
     if (pop > 0) emit_task(a, 0, 0, own);
   }
 
-  // first_iteration: every query against its own leaf
+  // first_iteration: every query against its own leaf.  Consecutive
+  // queries mostly share the leaf: the previous query's list after this
+  // pass holds k objects of the same leaf, so (when they exclude this
+  // issuer) they bound this query's k-th own-leaf distance by the triangle
+  // inequality, d <= d_prev(k) + |q - q_prev|.  Padded by 2^-30 relative
+  // (far above the rounding of any term), the bound only filters objects
+  // and chunks that cannot be among the k nearest of the leaf, so the list
+  // after the pass -- and the navigation threshold taken from it
+  // (engine.py:415) -- is exactly the reference's.
+  double p_kd = DINF, p_x = 0.0, p_y = 0.0;
+  long long p_id = IDMAX;  // this lane's entry of the previous list
+  uint32_t p_own = 0xffffffffu;
   for (int j = 0; j < nb; j++) {
     const double jx = __shfl_sync(FULL, qx, j), jy = __shfl_sync(FULL, qy, j);
     const long long jme = __shfl_sync(FULL, me, j);
     const uint32_t jown = __shfl_sync(FULL, own, j);
+    double cap = DINF;
+    if (KPL == 1 && jown == p_own && p_kd < DINF && !__any_sync(FULL, p_id == jme)) {
+      const double dx = jx - p_x, dy = jy - p_y;
+      const double rr = sqrt(p_kd) + sqrt(dx * dx + dy * dy);
+      cap = rr * rr * (1.0 + 0x1p-30) + 0x1p-1000;
+    }
     List<KPL> L;
 #pragma unroll
     for (int s = 0; s < KPL; s++) {
@@ -852,7 +881,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
       L.id[s] = IDMAX;
     }
     if constexpr (KPL == 1)
-      visit_leaf<KPL>(L, k, (int)jown, jx, jy, jme, a, lane, true);
+      visit_leaf<KPL>(L, k, (int)jown, jx, jy, jme, a, lane, true, cap);
     else
       visit_leaf_buf<KPL>(L, k, (int)jown, jx, jy, jme, a, lane, bufd, bufi, sd + j * N, si + j * N,
                           true);
@@ -860,6 +889,11 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
     long long ki;
     list_kth<KPL>(L, k, kd, ki);
     if (lane == j) thr = kd;
+    p_kd = kd;
+    p_x = jx;
+    p_y = jy;
+    p_id = L.id[0];
+    p_own = jown;
     if constexpr (ROWS) {
       const int64_t o = (int64_t)__shfl_sync(FULL, qrow, j) * k;
       row_store(L, a.out_dist + o, a.out_nids + o, k, lane);
