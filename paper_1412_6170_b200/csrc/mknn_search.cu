@@ -961,7 +961,25 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
   }
 
   // _emit: canonical order already; sqrt correctly rounded (engine.py:706)
-  for (int j = 0; j < nb; j++) {
+  if constexpr (ROWS && KPL == 1) {
+    // rows in the output: lane j turns row j around; the lanes walk the k
+    // entries together, so 32 rows' loads are in flight at once
+    const bool own_row = lane < nb;
+    const int64_t o = (int64_t)qrow * k;
+    int len = 0;
+    const unsigned long long pol = l2_evict_last();
+    for (int e = 0; e < k; e++) {
+      if (own_row) {
+        const double d = ld_keep(a.out_dist + o + e, pol);
+        if (d < DINF) {
+          len++;
+          __stcs(&a.out_dist[o + e], __dsqrt_rn(d));
+        }
+      }
+    }
+    if (own_row) a.out_len[qrow] = len;
+  }
+  for (int j = 0; j < nb && !(ROWS && KPL == 1); j++) {
     const uint32_t jq = __shfl_sync(FULL, q, j);
     const uint32_t row = ROWS ? __shfl_sync(FULL, qrow, j) : __ldg(&a.q_row[jq]);
     List<KPL> L;
