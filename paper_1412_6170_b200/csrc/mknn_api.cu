@@ -172,6 +172,7 @@ struct PinBlock {
   unsigned long long cnt[8];
   int64_t mm[2];
   int64_t total;
+  int32_t dup;
   uint32_t hist[2][HIST];
 };
 
@@ -187,6 +188,7 @@ struct mknn_engine {
   bool have_index = false;
   bool last_tick_ok = false;
   int issuer_bits = -1;        // issuer-id bits of the last tick (plans the row sort)
+  bool issuer_dups = false;    // a batch repeated an issuer id: rows by radix sort from then on
   cudaStream_t copy_stream = nullptr;  // result slices device -> host
   cudaEvent_t slice_ev[N_SLICES] = {};
   cudaEvent_t q_ready = nullptr;  // host query batch staged on copy_stream
@@ -386,6 +388,7 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
   }
   const int64_t ncap = int64_t(1) << (2 * h->cfg.l_max);
   size_t sb = std::max({scan_scratch_bytes(ncap + 2), scan_scratch_bytes(n + ncap + 2),
+                        scan_scratch_bytes((int64_t(1) << 22) + 2),  // issuer bitmap words
                         scan_scratch_bytes(std::max<int64_t>(nq, 1) + 1),
                         radix_scratch_bytes(std::max<int64_t>(nq, 1))});
   if ((rc = h->scratch.ensure(sb + 1024))) return h->set_err(rc);
@@ -445,7 +448,7 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
     h->q_pending = false;
   }
   if ((rc = queries_index(h->dq, h->st, h->ix, h->r, qi, qx, qy, nq, h->h_n_sub, h->issuer_bits,
-                          &bits_used, o.qids, h->scratch.p, s)))
+                          &bits_used, !h->issuer_dups, o.qids, h->scratch.p, s)))
     return h->set_err(rc);
   MKNN_CUDA_OK(cudaEventRecord(h->ev[3], s));
 
@@ -576,6 +579,9 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
   pb.mm[0] = pb.mm[1] = 0;
   if (nq) MKNN_CUDA_OK(cudaMemcpyAsync(pb.mm, h->dq.minmax, sizeof(pb.mm), cudaMemcpyDeviceToHost, s));
   MKNN_CUDA_OK(cudaMemcpyAsync(&pb.total, o.offsets + nq, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  pb.dup = 0;
+  if (nq && h->dq.dup)
+    MKNN_CUDA_OK(cudaMemcpyAsync(&pb.dup, h->dq.dup, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   const int64_t hpre = std::min<int64_t>(h->hist_cap, PinBlock::HIST);
   if (nq)
     for (int d = 0; d < 2; d++)
@@ -594,7 +600,8 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
     // tick's range needs more bits the row order is wrong -> redo the tick
     const int need = issuer_bits(mm[0], mm[1]);
     h->issuer_bits = need;
-    if (need > bits_used) {
+    if (pb.dup && need <= bits_used) h->issuer_dups = true;  // a repeated issuer id
+    if (need > bits_used || pb.dup) {
       *retry = true;
       h->retry_rebuild = rebuild;
       return 0;
@@ -933,6 +940,7 @@ void mknn_destroy(mknn_engine* h) {
                   h->st.box, h->st.crange, h->st.cnt, h->st.kstart, 
                   h->dq.leaf, h->dq.qkey, h->dq.order, h->dq.row,
                   h->dq.keys, h->dq.keys_alt, h->dq.vals, h->dq.vals_alt, h->dq.minmax,
+                  h->dq.bm, h->dq.bm_cnt, h->dq.bm_pre, h->dq.dup,
                   h->in_ids, h->in_x, h->in_y, h->in_qi, h->in_qx, h->in_qy, h->out_len,
                   h->out_nids, h->out_dist, h->c_nids, h->c_dist, h->offsets, h->out_qids,
                   h->stats, h->counters, h->hist, h->snap_ids, h->snap_x, h->snap_y, h->hkeys,

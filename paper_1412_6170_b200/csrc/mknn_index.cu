@@ -510,6 +510,46 @@ __global__ void k_issuer_rows(const uint64_t* __restrict__ keys, const uint32_t*
   }
 }
 
+// Row order without a sort when the issuers are distinct: one bit per id of
+// [min, min + 2^bits) marks the batch's ids; a query's row is the number of
+// marked ids below its own (popcount prefix over words) -- the stable issuer
+// rank of engine.py:713 when no id repeats.  A repeated id (or an id beyond
+// the planned range) raises *dup and the tick is redone with the radix sort.
+__global__ void k_issuer_mark(const long long* __restrict__ qi, int64_t nq,
+                              const int64_t* __restrict__ mm, uint64_t span,
+                              uint32_t* __restrict__ bm, int32_t* __restrict__ dup) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nq) {
+    const uint64_t key = (uint64_t)qi[i] - (uint64_t)mm[0];
+    if (key >= span) {
+      *dup = 1;
+      return;
+    }
+    const uint32_t bit = 1u << (key & 31);
+    if (atomicOr(&bm[key >> 5], bit) & bit) *dup = 1;
+  }
+}
+
+__global__ void k_word_popc(const uint32_t* __restrict__ bm, int64_t nw, int32_t* __restrict__ cnt) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w < nw) cnt[w] = __popc(bm[w]);
+}
+
+__global__ void k_issuer_rank(const long long* __restrict__ qi, int64_t nq,
+                              const int64_t* __restrict__ mm, uint64_t span,
+                              const uint32_t* __restrict__ bm, const int32_t* __restrict__ pre,
+                              uint32_t* __restrict__ row, long long* __restrict__ out_qids) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nq) {
+    const uint64_t key = (uint64_t)qi[i] - (uint64_t)mm[0];
+    if (key >= span) return;  // the tick is redone (dup flag)
+    const int64_t w = (int64_t)(key >> 5);
+    const uint32_t r = (uint32_t)pre[w] + (uint32_t)__popc(bm[w] & ((1u << (key & 31)) - 1u));
+    row[i] = r;
+    if (out_qids && r < (uint64_t)nq) out_qids[r] = qi[i];
+  }
+}
+
 inline unsigned grid_stride_blocks(int64_t n) {
   int64_t b = (n + TPB - 1) / TPB;
   return (unsigned)std::min<int64_t>(std::max<int64_t>(b, 1), 148 * 16);
@@ -731,7 +771,7 @@ int issuer_bits(int64_t lo, int64_t hi) {
 
 int queries_index(DevQueries& dq, DevStore& st, const DevIndex& ix, const Region& r,
                   const long long* qi, const double* qx, const double* qy, int64_t nq,
-                  int64_t n_sub, int plan_bits, int* bits_used, long long* out_qids, void* scratch,
+                  int64_t n_sub, int plan_bits, int* bits_used, bool bitmap, long long* out_qids, void* scratch,
                   cudaStream_t s) {
   *bits_used = 0;
   if (nq == 0) return 0;
@@ -759,6 +799,34 @@ int queries_index(DevQueries& dq, DevStore& st, const DevIndex& ix, const Region
     bits = issuer_bits(mm[0], mm[1]);
   }
   *bits_used = bits;
+  if (bitmap && bits <= 27) {  // distinct issuers expected: rank by bitmap (<= 16 MB)
+    const uint64_t span = 1ull << bits;
+    const int64_t nw = (int64_t)((span + 31) >> 5);
+    if (nw + 1 > dq.bm_cap || !dq.dup) {
+      cudaFree(dq.bm);
+      cudaFree(dq.bm_cnt);
+      cudaFree(dq.bm_pre);
+      if (!dq.dup) MKNN_CUDA_OK(cudaMalloc(&dq.dup, sizeof(int32_t)));
+      dq.bm_cap = 0;
+      const int64_t c = std::max<int64_t>(nw + 1, 1024);
+      MKNN_CUDA_OK(cudaMalloc(&dq.bm, sizeof(uint32_t) * c));
+      MKNN_CUDA_OK(cudaMalloc(&dq.bm_cnt, sizeof(int32_t) * c));
+      MKNN_CUDA_OK(cudaMalloc(&dq.bm_pre, sizeof(int32_t) * (c + 1)));
+      dq.bm_cap = c;
+    }
+    MKNN_CUDA_OK(cudaMemsetAsync(dq.bm, 0, sizeof(uint32_t) * nw, s));
+    MKNN_CUDA_OK(cudaMemsetAsync(dq.dup, 0, sizeof(int32_t), s));
+    MKNN_LAUNCH k_issuer_mark<<<blocks_for(nq), TPB, 0, s>>>(qi, nq, dq.minmax, span, dq.bm, dq.dup);
+    MKNN_LAUNCH k_word_popc<<<blocks_for(nw), TPB, 0, s>>>(dq.bm, nw, dq.bm_cnt);
+    MKNN_CUDA_OK(cudaGetLastError());
+    rc = exclusive_scan_i32(dq.bm_cnt, dq.bm_pre, nw, scratch, s);
+    if (rc) return rc;
+    MKNN_LAUNCH k_issuer_rank<<<blocks_for(nq), TPB, 0, s>>>(qi, nq, dq.minmax, span, dq.bm, dq.bm_pre,
+                                                            dq.row, out_qids);
+    MKNN_CUDA_OK(cudaGetLastError());
+    return 0;
+  }
+  if (dq.dup) MKNN_CUDA_OK(cudaMemsetAsync(dq.dup, 0, sizeof(int32_t), s));
   MKNN_LAUNCH k_issuer_keys<<<blocks_for(nq), TPB, 0, s>>>(qi, nq, dq.minmax, dq.keys, dq.vals);
   MKNN_CUDA_OK(cudaGetLastError());
   bool alt = false;

@@ -181,6 +181,12 @@ struct DevQueries {
   uint32_t* vals_alt = nullptr;
   int64_t* minmax = nullptr;    // device [2]
   int64_t cap = 0;
+  // issuer rank by bitmap (distinct issuers): one bit per id of the range
+  uint32_t* bm = nullptr;
+  int32_t* bm_cnt = nullptr;    // popcount per word, then its exclusive scan
+  int32_t* bm_pre = nullptr;
+  int64_t bm_cap = 0;           // words
+  int32_t* dup = nullptr;       // device flag: an issuer id occurs twice (or left the range)
 };
 
 // uses st.sub_cnt / st.sub_start as its counting-sort tables
@@ -188,7 +194,7 @@ struct DevQueries {
 // sync); *bits_used receives the bits actually sorted on
 int queries_index(DevQueries& dq, DevStore& st, const DevIndex& ix, const Region& r,
                   const long long* qi, const double* qx, const double* qy, int64_t nq,
-                  int64_t n_sub, int plan_bits, int* bits_used, long long* out_qids, void* scratch,
+                  int64_t n_sub, int plan_bits, int* bits_used, bool bitmap, long long* out_qids, void* scratch,
                   cudaStream_t s);
 // bits of the issuer-id range [lo, hi]
 int issuer_bits(int64_t lo, int64_t hi);
