@@ -128,6 +128,28 @@ def test_duplicate_issuers_keep_input_order():
     assert_same(res, orc.brute_force_knn(ids, x, y, qi, qx, qy, 7))
 
 
+@pytest.mark.parametrize("sliced", [False, True])
+def test_issuer_rows_distinct_then_repeated(sliced):
+    """Row order (engine.py:713) by the issuer bitmap rank while the issuers
+    are distinct; a later batch that repeats an id is redone with the stable
+    radix sort (duplicates keep their input order), and distinct batches
+    after it stay exact.  The sliced case runs the host tick's row slices."""
+    rng = np.random.default_rng(9)
+    n = 120_000 if sliced else 6_000
+    nq = 70_000 if sliced else 900
+    x = rng.uniform(0, 300, n)
+    y = rng.uniform(0, 300, n)
+    ids = rng.permutation(10 * n).astype(np.int64)[:n] + 17
+    with Engine(EngineConfig(k=6, region=Rect.square(300.0), th_quad=24)) as eng:
+        for t, dup in enumerate([False, False, True, False, True]):
+            sel = rng.choice(n, nq, replace=False)
+            qi, qx, qy = ids[sel].copy(), x[sel], y[sel]
+            if dup:  # repeat some issuers (different positions)
+                qi[1::7] = qi[0:-1:7][: len(qi[1::7])]
+            res = eng.process_tick(ids, x, y, qi, qx, qy)
+            assert_same(res, orc.brute_force_knn(ids, x, y, qi, qx, qy, 6))
+
+
 def test_delta_path_equals_full_snapshot():
     """load + update + query == process_tick on the carried-forward snapshot
     (datasets.py:136-148)."""
