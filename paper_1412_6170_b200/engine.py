@@ -143,6 +143,25 @@ def _tptr(t) -> int:
 
 _CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the legacy NULL stream as a handle
 
+_POOL = None
+
+
+def _parallel_fill(fn, n: int, min_chunk: int = 1 << 17) -> None:
+    """fn(lo, hi) over [0, n) in chunks on a small thread pool (numpy
+    releases the GIL): the 8 MB offsets array of a 1M-query tick costs ~1 ms
+    on one host core, most of the host time outside the C call."""
+    global _POOL
+    parts = min(8, max(1, n // min_chunk))
+    if parts == 1:
+        fn(0, n)
+        return
+    if _POOL is None:
+        import concurrent.futures
+
+        _POOL = concurrent.futures.ThreadPoolExecutor(max_workers=8)
+    step = (n + parts - 1) // parts
+    list(_POOL.map(lambda i: fn(i * step, min(n, (i + 1) * step)), range(parts)))
+
 
 class Engine:
     """Stateful tick processor: owns the device index, the rebuild history
@@ -309,7 +328,8 @@ class Engine:
         if n_results == nq * k:  # every row full: the CSR is the padded rows
             if len(self._ramp) != nq + 1:
                 self._ramp = np.arange(nq + 1, dtype=np.int64)
-            np.multiply(self._ramp, k, out=offsets)
+            _parallel_fill(lambda lo, hi: np.multiply(self._ramp[lo:hi], k, out=offsets[lo:hi]),
+                           nq + 1)
         else:
             offsets[0] = 0
             np.cumsum(lens, out=offsets[1:])
