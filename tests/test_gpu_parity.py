@@ -193,6 +193,38 @@ def test_device_tensors_path():
     assert out["distances"][:nres].cpu().numpy().tobytes() == host.distances.tobytes()
 
 
+def test_device_calls_follow_the_torch_stream():
+    """Tensors produced on a side stream (async pinned copies, a sleep kernel
+    ahead of them) feed update/query_device/tick_device on that stream: the
+    engine follows torch's current stream, so it never reads them early."""
+    snap = synth.place(40_000, "gaussian", seed=6, hotspots=4)
+    qi, qx, qy = synth.queries(snap, 4000, seed=6)
+    ups = synth.updates(snap, 0.1, 1, seed=6)
+    side = torch.cuda.Stream()
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+
+    def dev(a):
+        torch.cuda._sleep(2_000_000)  # keep the stream busy ahead of the copy
+        return pin(a).to("cuda", non_blocking=True)
+
+    want0 = orc.brute_force_knn(snap.ids, snap.x, snap.y, qi, qx, qy, 12)
+    after = synth.Snapshot(snap.ids.copy(), snap.x.copy(), snap.y.copy())
+    synth.apply_updates(after, *ups)
+    want1 = orc.brute_force_knn(after.ids, after.x, after.y, qi, qx, qy, 12)
+    with Engine(EngineConfig(k=12, region=synth.REGION)) as eng, torch.cuda.stream(side):
+        d = [dev(a) for a in (snap.ids, snap.x, snap.y, qi, qx, qy)]
+        out = eng.tick_device(*d)
+        n = out["n_results"]
+        got = out["neighbour_ids"][:n].cpu().numpy()
+        assert np.array_equal(got, want0.neighbour_ids)
+        eng.update(*[dev(a) for a in (snap.ids, snap.x, snap.y)])
+        eng.update(*[dev(a) for a in ups])
+        out = eng.query_device(*[dev(a) for a in (qi, qx, qy)])
+        n = out["n_results"]
+        assert np.array_equal(out["neighbour_ids"][:n].cpu().numpy(), want1.neighbour_ids)
+        assert out["distances"][:n].cpu().numpy().tobytes() == want1.distances.tobytes()
+
+
 def test_audit_pruning_finds_no_violations():
     snap = synth.place(20_000, "gaussian", seed=4, hotspots=5)
     qi, qx, qy = synth.queries(snap, 2000, seed=4)
