@@ -409,6 +409,11 @@ def main() -> int:
             "T": int(T_records), "t_launch_us": t_search_s * 1e6,
             "tick_B_alg": int(tick_bytes),
             "tick_frac": tick_bytes / (ms_per_step / 1e3) / 1e9 / peak,
+            # SURVEY §8(d) floor: T := n (every object streamed once)
+            "tick_B_min": int(tick_bytes - 24 * T_records + 24 * wl["n"]),
+            # secondary figures of the same kernel from its ncu capture
+            "fp64_pipe_pct": prof.get("fp64_pipe_pct") if traffic else None,
+            "issue_active_pct": prof.get("issue_active_pct") if traffic else None,
         },
         "clocks": clk.summary(),
         "tick_phases_us": {"build": m0.t_build_us, "index_objects": m0.t_index_objects_us,
