@@ -133,12 +133,24 @@ __global__ void k_update_apply(const long long* __restrict__ ids, const double* 
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nu;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t s = slot_of[i];
+    bool first = false;
     if (winner[s] == (int32_t)i) {
       sids[s] = ids[i];
       sx[s] = x[i];
       sy[s] = y[i];
       // slots changed since the store was built (once per slot and epoch)
-      if (atomicExch(&mark[s], epoch) != epoch) moved[atomicAdd(n_moved, 1)] = s;
+      first = atomicExch(&mark[s], epoch) != epoch;
+    }
+    // one counter atomic per warp (10M updates on one address serialise)
+    const unsigned act = __activemask();
+    const unsigned want = __ballot_sync(act, first);
+    if (want) {
+      const int lane = threadIdx.x & 31;
+      const int leader = __ffs(want) - 1;
+      int32_t base = 0;
+      if (lane == leader) base = atomicAdd(n_moved, __popc(want));
+      base = __shfl_sync(act, base, leader);
+      if (first) moved[base + __popc(want & ((1u << lane) - 1u))] = s;
     }
   }
 }
