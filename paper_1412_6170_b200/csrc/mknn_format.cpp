@@ -25,18 +25,22 @@ int64_t format_rows(int64_t tick, int64_t r0, int64_t r1, const int64_t* qids,
   for (int64_t r = r0; r < r1; r++) {
     for (int64_t e = offsets[r]; e < offsets[r + 1]; e++) {
       // std::to_chars(general, 9) is printf's "%.9g", exactly rounded
+      // a line is at most 4 x 20 digits + 16 + 5 separators < sizeof(line);
+      // the checks keep every write provably inside the buffer
       char* p = line;
-      char* const end = line + sizeof(line);
-      p = std::to_chars(p, end, (long long)tick).ptr;
-      *p++ = ',';
-      p = std::to_chars(p, end, (long long)qids[r]).ptr;
-      *p++ = ',';
-      p = std::to_chars(p, end, (long long)(e - offsets[r])).ptr;
-      *p++ = ',';
-      p = std::to_chars(p, end, (long long)nids[e]).ptr;
-      *p++ = ',';
-      p = std::to_chars(p, end, dist[e], std::chars_format::general, 9).ptr;
-      *p++ = '\n';
+      char* const end = line + sizeof(line) - 1;
+      auto field = [&](auto r, char sep) {
+        if (r.ec != std::errc() || r.ptr >= end) return false;
+        p = r.ptr;
+        *p++ = sep;
+        return true;
+      };
+      if (!field(std::to_chars(p, end, (long long)tick), ',') ||
+          !field(std::to_chars(p, end, (long long)qids[r]), ',') ||
+          !field(std::to_chars(p, end, (long long)(e - offsets[r])), ',') ||
+          !field(std::to_chars(p, end, (long long)nids[e]), ',') ||
+          !field(std::to_chars(p, end, dist[e], std::chars_format::general, 9), '\n'))
+        return -1;
       const int64_t n = p - line;
       if (w + n > cap) return -1;
       memcpy(out + w, line, (size_t)n);
