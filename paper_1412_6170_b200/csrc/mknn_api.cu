@@ -55,6 +55,13 @@ struct Buf {
 
 constexpr long long HASH_EMPTY = (long long)0x8000000000000000ULL;
 
+// one probe = one 16-byte slot (key and slot index in the same sector)
+struct __align__(16) HashSlot {
+  long long key;
+  int32_t val;
+  int32_t pad;
+};
+
 __device__ __forceinline__ uint64_t hash64(uint64_t x) {
   x ^= x >> 33;
   x *= 0xff51afd7ed558ccdULL;
@@ -77,25 +84,25 @@ __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
 
 // id -> slot map (open addressing, linear probing).  A new id claims the
 // next snapshot slot; concurrent inserts of one id wait for the winner.
-__device__ int32_t hash_find_or_insert(long long* keys, int32_t* vals, uint64_t mask, long long id,
+__device__ int32_t hash_find_or_insert(HashSlot* ht, uint64_t mask, long long id,
                                        int32_t* n_snap, bool insert_new, int32_t fixed_slot) {
   uint64_t h = hash64((uint64_t)id) & mask;
   for (;;) {
-    long long cur = keys[h];
+    long long cur = ht[h].key;
     if (cur == id) {
       int32_t v;
-      while ((v = ((volatile int32_t*)vals)[h]) < 0) {
+      while ((v = ((volatile int32_t*)&ht[h].val)[0]) < 0) {
       }
       return v;
     }
     if (cur == HASH_EMPTY) {
-      const long long prev = (long long)atomicCAS((unsigned long long*)&keys[h],
+      const long long prev = (long long)atomicCAS((unsigned long long*)&ht[h].key,
                                                   (unsigned long long)HASH_EMPTY,
                                                   (unsigned long long)id);
       if (prev == HASH_EMPTY) {
         const int32_t slot = insert_new ? (fixed_slot >= 0 ? fixed_slot : atomicAdd(n_snap, 1)) : -1;
         __threadfence();
-        atomicExch(&vals[h], slot);
+        atomicExch(&ht[h].val, slot);
         return slot;
       }
       if (prev == id) continue;  // lost the race to the same id: wait above
@@ -104,22 +111,28 @@ __device__ int32_t hash_find_or_insert(long long* keys, int32_t* vals, uint64_t 
   }
 }
 
-__global__ void k_hash_load(const long long* __restrict__ ids, int64_t n, long long* keys,
-                            int32_t* vals, uint64_t mask, int32_t* winner) {
+__global__ void k_fill_slots(HashSlot* ht, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    ht[i] = HashSlot{HASH_EMPTY, -1, 0};
+}
+
+__global__ void k_hash_load(const long long* __restrict__ ids, int64_t n, HashSlot* ht,
+                            uint64_t mask, int32_t* winner) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     // duplicate ids inside a snapshot: the first slot keeps the mapping
-    hash_find_or_insert(keys, vals, mask, ids[i], nullptr, true, (int32_t)i);
+    hash_find_or_insert(ht, mask, ids[i], nullptr, true, (int32_t)i);
   }
 }
 
 // last update per id wins (datasets.py:130-131): winner[slot] = max index
-__global__ void k_update_claim(const long long* __restrict__ ids, int64_t nu, long long* keys,
-                               int32_t* vals, uint64_t mask, int32_t* n_snap, int32_t* winner,
+__global__ void k_update_claim(const long long* __restrict__ ids, int64_t nu, HashSlot* ht,
+                               uint64_t mask, int32_t* n_snap, int32_t* winner,
                                int32_t* slot_of) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nu;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t s = hash_find_or_insert(keys, vals, mask, ids[i], n_snap, true, -1);
+    const int32_t s = hash_find_or_insert(ht, mask, ids[i], n_snap, true, -1);
     slot_of[i] = s;
     atomicMax(&winner[s], (int32_t)i);
   }
@@ -236,7 +249,7 @@ struct mknn_engine {
   // persistent snapshot (delta path)
   long long* snap_ids = nullptr; double *snap_x = nullptr, *snap_y = nullptr; int64_t cap_snap = 0;
   int64_t n_snap = 0;
-  long long* hkeys = nullptr; int32_t* hvals = nullptr; int64_t hcap = 0;
+  HashSlot* ht = nullptr; int64_t hcap = 0;  // id -> snapshot slot
   int32_t* winner = nullptr; int64_t cap_winner = 0;
   // incremental store (delta ticks): slots moved since the store was built
   int32_t* mark = nullptr;     // per slot: epoch of its last recorded move
@@ -796,7 +809,7 @@ int stage_queries(mknn_engine* h, int64_t nq, const int64_t* qi, const double* q
 
 // ----------------------------------------------------------- delta snapshot
 int snap_reserve(mknn_engine* h, int64_t want) {
-  if (want <= h->cap_snap && h->hkeys) return 0;
+  if (want <= h->cap_snap && h->ht) return 0;
   const int64_t nc = std::max<int64_t>(want, std::max<int64_t>(h->cap_snap * 3 / 2, 1024));
   cudaStream_t s = h->stream;
   long long* ni = nullptr;
@@ -820,11 +833,9 @@ int snap_reserve(mknn_engine* h, int64_t want) {
   // rehash at <= 50 % load
   int64_t hc = 1;
   while (hc < 2 * nc) hc <<= 1;
-  cudaFree(h->hkeys);
-  cudaFree(h->hvals);
+  cudaFree(h->ht);
   cudaFree(h->winner);
-  MKNN_CUDA_OK(cudaMalloc(&h->hkeys, sizeof(long long) * hc));
-  MKNN_CUDA_OK(cudaMalloc(&h->hvals, sizeof(int32_t) * hc));
+  MKNN_CUDA_OK(cudaMalloc(&h->ht, sizeof(HashSlot) * hc));
   MKNN_CUDA_OK(cudaMalloc(&h->winner, sizeof(int32_t) * nc));
   cudaFree(h->mark);
   cudaFree(h->moved);
@@ -838,12 +849,11 @@ int snap_reserve(mknn_engine* h, int64_t want) {
   h->hcap = hc;
   h->cap_winner = nc;
   if (!h->d_nsnap) MKNN_CUDA_OK(cudaMalloc(&h->d_nsnap, sizeof(int32_t)));
-  MKNN_LAUNCH k_fill_i64<<<gs_blocks(hc), 256, 0, s>>>(h->hkeys, hc, HASH_EMPTY);
-  MKNN_LAUNCH k_fill_i32<<<gs_blocks(hc), 256, 0, s>>>(h->hvals, hc, -1);
+  MKNN_LAUNCH k_fill_slots<<<gs_blocks(hc), 256, 0, s>>>(h->ht, hc);
   MKNN_LAUNCH k_fill_i32<<<gs_blocks(nc), 256, 0, s>>>(h->winner, nc, -1);
   if (h->n_snap)
-    MKNN_LAUNCH k_hash_load<<<gs_blocks(h->n_snap), 256, 0, s>>>(h->snap_ids, h->n_snap, h->hkeys, h->hvals,
-                                                       (uint64_t)(hc - 1), h->winner);
+    MKNN_LAUNCH k_hash_load<<<gs_blocks(h->n_snap), 256, 0, s>>>(h->snap_ids, h->n_snap, h->ht,
+                                                                 (uint64_t)(hc - 1), h->winner);
   MKNN_CUDA_OK(cudaGetLastError());
   return 0;
 }
@@ -859,11 +869,10 @@ int snap_load_dev(mknn_engine* h, int64_t n, const long long* ids, const double*
     MKNN_CUDA_OK(cudaMemcpyAsync(h->snap_x, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     MKNN_CUDA_OK(cudaMemcpyAsync(h->snap_y, y, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   }
-  MKNN_LAUNCH k_fill_i64<<<gs_blocks(h->hcap), 256, 0, s>>>(h->hkeys, h->hcap, HASH_EMPTY);
-  MKNN_LAUNCH k_fill_i32<<<gs_blocks(h->hcap), 256, 0, s>>>(h->hvals, h->hcap, -1);
+  MKNN_LAUNCH k_fill_slots<<<gs_blocks(h->hcap), 256, 0, s>>>(h->ht, h->hcap);
   if (n)
-    MKNN_LAUNCH k_hash_load<<<gs_blocks(n), 256, 0, s>>>(h->snap_ids, n, h->hkeys, h->hvals,
-                                               (uint64_t)(h->hcap - 1), h->winner);
+    MKNN_LAUNCH k_hash_load<<<gs_blocks(n), 256, 0, s>>>(h->snap_ids, n, h->ht,
+                                                         (uint64_t)(h->hcap - 1), h->winner);
   MKNN_CUDA_OK(cudaGetLastError());
   h->n_snap = n;
   return 0;
@@ -877,7 +886,7 @@ int snap_update_dev(mknn_engine* h, int64_t nu, const long long* ids, const doub
   cudaStream_t s = h->stream;
   const int32_t ns = (int32_t)h->n_snap;
   MKNN_CUDA_OK(cudaMemcpyAsync(h->d_nsnap, &ns, sizeof(int32_t), cudaMemcpyHostToDevice, s));
-  MKNN_LAUNCH k_update_claim<<<gs_blocks(nu), 256, 0, s>>>(ids, nu, h->hkeys, h->hvals, (uint64_t)(h->hcap - 1),
+  MKNN_LAUNCH k_update_claim<<<gs_blocks(nu), 256, 0, s>>>(ids, nu, h->ht, (uint64_t)(h->hcap - 1),
                                                h->d_nsnap, h->winner, h->slot_of);
   MKNN_LAUNCH k_update_apply<<<gs_blocks(nu), 256, 0, s>>>(ids, x, y, nu, h->slot_of, h->winner, h->snap_ids,
                                                h->snap_x, h->snap_y, h->mark, h->epoch, h->moved,
@@ -955,8 +964,8 @@ void mknn_destroy(mknn_engine* h) {
                   h->dq.bm, h->dq.bm_cnt, h->dq.bm_pre, h->dq.dup,
                   h->in_ids, h->in_x, h->in_y, h->in_qi, h->in_qx, h->in_qy, h->out_len,
                   h->out_nids, h->out_dist, h->c_nids, h->c_dist, h->offsets, h->out_qids,
-                  h->stats, h->counters, h->hist, h->snap_ids, h->snap_x, h->snap_y, h->hkeys,
-                  h->hvals, h->winner, h->slot_of, h->d_nsnap, h->up_ids, h->up_x, h->up_y,
+                  h->stats, h->counters, h->hist, h->snap_ids, h->snap_x, h->snap_y, h->ht,
+                  h->winner, h->slot_of, h->d_nsnap, h->up_ids, h->up_x, h->up_y,
                   h->tk, h->tk_alt, h->tk_cnt, h->tv, h->tv_alt, h->prof, h->mark, h->moved,
                   h->d_nmoved, h->clamped_total, h->st.kstart_alt, h->st.fill,
                   h->st.qcnt, h->st.qkstart, h->st.rmflag, h->st.rm_before, h->st.mkey};
