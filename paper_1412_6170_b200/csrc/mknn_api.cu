@@ -175,7 +175,7 @@ __global__ void k_update_reset(int64_t nu, const int32_t* __restrict__ slot_of, 
 }
 
 inline unsigned gs_blocks(int64_t n) {
-  return (unsigned)std::min<int64_t>(std::max<int64_t>((n + 255) / 256, 1), 148 * 16);
+  return (unsigned)std::min<int64_t>(std::max<int64_t>((n + 255) / 256, 1), 148 * 256);
 }
 
 int64_t us_between(cudaEvent_t a, cudaEvent_t b) {

@@ -550,9 +550,9 @@ __global__ void k_issuer_rank(const long long* __restrict__ qi, int64_t nq,
   }
 }
 
-inline unsigned grid_stride_blocks(int64_t n) {
+inline unsigned grid_stride_blocks(int64_t n, int64_t max_blocks = 148 * 16) {
   int64_t b = (n + TPB - 1) / TPB;
-  return (unsigned)std::min<int64_t>(std::max<int64_t>(b, 1), 148 * 16);
+  return (unsigned)std::min<int64_t>(std::max<int64_t>(b, 1), max_blocks);
 }
 
 }  // namespace
@@ -725,7 +725,7 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
   int rc = exclusive_scan_i32(st.cnt, st.kstart, n_sub, scratch, s);
   if (rc) return rc;
   if (n > 0)
-    MKNN_LAUNCH k_final_scatter<<<grid_stride_blocks(n), TPB, 0, s>>>(st.rec, n, st.kstart, st.cnt,
+    MKNN_LAUNCH k_final_scatter<<<grid_stride_blocks(n, 148 * 64), TPB, 0, s>>>(st.rec, n, st.kstart, st.cnt,
                                                                      st.obj);
   MKNN_CUDA_OK(cudaGetLastError());
   return store_finish(st, ix, n, n_leaves, scratch, s);
