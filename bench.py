@@ -28,11 +28,17 @@ k=32; synthetic data from the reference generator's placement draws
   counted on device in one extra untimed instrumented step), divided by the
   kernel's CUDA-event time (engine metrics t_loop_us).
 * cpu_baseline: the C port of the reference engine (oracle/, OpenMP, all host
-  threads) on a bounded sample, scaled to one tick.
-* --gpus N>1 (torchrun): weak scaling, each rank answers 1M queries of its
-  own against the replicated snapshot; the snapshot (or the tick's updates)
-  arrive as 1/N slices per rank and are all-gathered over NCCL every step
-  (sharded.py).
+  threads) on a steady-state tick (index reused) with a bounded query sample,
+  scaled to one tick.
+* --impl reference: the same port, every step a full steady-state tick with
+  all queries, plus the threads=1 port figure and the unmodified Python
+  reference (mknn.Engine from baseline/_ref) on bounded samples.
+* --gpus N>1 (torchrun): strong scaling by default (the workload's query
+  batch split over the ranks, BASELINE configs[3]); --scaling weak gives
+  every rank the full batch.  The snapshot (or the tick's updates) arrive as
+  1/N slices per rank and are all-gathered over NCCL every step
+  (sharded.py); the replicated re-index and the query phase are reported
+  separately.
 """
 
 from __future__ import annotations
@@ -138,28 +144,80 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
 
 
-def cpu_port_tick_seconds(snap, qi, qx, qy, k, region, th, sample_q):
+def cpu_port_tick_seconds(snap, qi, qx, qy, k, region, th, sample_q, index=None):
     """The C port of the reference engine (oracle/, test infrastructure used
-    here only as the reported CPU baseline): index-only tick + a query
-    sample, scaled to the full query count."""
+    here only as the reported CPU baseline), as a steady-state tick: the
+    index built on an earlier tick is reused (engine.py:615-619), so a step
+    is index_objects + index_queries + the distance phases + emission.  The
+    query part runs on ``sample_q`` queries and is scaled to the tick.
+    Returns (seconds per tick, seconds of the object re-index, seconds of the
+    sampled tick, threads)."""
     from oracle import oracle as orc
 
-    t = time.perf_counter()
-    orc.engine_tick(snap.ids, snap.x, snap.y, qi[:0], qx[:0], qy[:0], k, region, th)
-    t_index = time.perf_counter() - t
-    t = time.perf_counter()
-    orc.engine_tick(snap.ids, snap.x, snap.y, qi[:sample_q], qx[:sample_q], qy[:sample_q], k,
-                    region, th)
-    t_sample = time.perf_counter() - t
+    own = index is None
+    if own:
+        index = orc.build_index(snap.x, snap.y, region, th, 10)
+    try:
+        t = time.perf_counter()
+        orc.engine_tick(snap.ids, snap.x, snap.y, qi[:0], qx[:0], qy[:0], k, region, th,
+                        index=index)
+        t_index = time.perf_counter() - t
+        if sample_q >= len(qi):
+            t = time.perf_counter()
+            orc.engine_tick(snap.ids, snap.x, snap.y, qi, qx, qy, k, region, th, index=index)
+            t_sample = time.perf_counter() - t
+            return t_sample, t_index, t_sample, orc.num_threads()
+        t = time.perf_counter()
+        orc.engine_tick(snap.ids, snap.x, snap.y, qi[:sample_q], qx[:sample_q], qy[:sample_q], k,
+                        region, th, index=index)
+        t_sample = time.perf_counter() - t
+    finally:
+        if own:
+            orc.free_index(index)
     per_q = max(t_sample - t_index, 0.0) / max(sample_q, 1)
     return t_index + per_q * len(qi), t_index, t_sample, orc.num_threads()
 
 
-def make_inputs(wl, world=1, rank=0):
+def python_reference_tick_seconds(snap, qi, qx, qy, k, region, sample_q, threads):
+    """The reference package itself (mknn.Engine from baseline/_ref, the
+    unmodified pure-Python/numpy engine, engine.py:557-701) on a steady-state
+    tick: a first tick builds the index, a 0-query tick times the per-tick
+    object re-index, a ``sample_q``-query tick the per-query part, scaled to
+    the full query count.  None when baseline/_ref is absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "mknn")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    from mknn import Engine as RefEngine, EngineConfig as RefConfig, Rect as RefRect
+
+    r = RefRect(region.x_lo, region.y_lo, region.x_hi, region.y_hi)
+    s = slice(0, sample_q)
+    with RefEngine(RefConfig(k=k, region=r, threads=threads)) as eng:
+        eng.process_tick(snap.ids, snap.x, snap.y, qi[:0], qx[:0], qy[:0])  # builds the index
+        t = time.perf_counter()
+        eng.process_tick(snap.ids, snap.x, snap.y, qi[:0], qx[:0], qy[:0])
+        t0 = time.perf_counter() - t
+        t = time.perf_counter()
+        eng.process_tick(snap.ids, snap.x, snap.y, qi[s], qx[s], qy[s])
+        t1 = time.perf_counter() - t
+        assert eng.last_metrics.rebuild_flag == 0
+    per_q = max(t1 - t0, 0.0) / max(min(sample_q, len(qi)), 1)
+    return dict(value=len(qi) / (t0 + per_q * len(qi)), unit=UNIT, cores=threads,
+                kind="reference",
+                sample=f"mknn.Engine (baseline/_ref) threads={threads}: steady-state tick over "
+                       f"{len(snap.ids)} objects with 0 queries ({t0:.2f} s) and {sample_q} "
+                       f"queries ({t1:.2f} s), scaled to {len(qi)} queries")
+
+
+def make_inputs(wl, world=1, rank=0, strong=True):
+    """The workload's snapshot and this rank's queries: strong scaling
+    splits the workload's query batch over the ranks, weak scaling gives
+    every rank a batch of that size."""
     from paper_1412_6170_b200 import synth
 
     snap = synth.place(wl["n"], wl["dist"], seed=wl["seed"])
-    nq_total = min(wl["nq"] * world, wl["n"])
+    nq_total = min(wl["nq"] * (1 if strong else world), wl["n"])
     qi, qx, qy = synth.queries(snap, nq_total, seed=wl["seed"])
     if world > 1:
         from paper_1412_6170_b200.sharded import shard_queries
@@ -169,9 +227,28 @@ def make_inputs(wl, world=1, rank=0):
     return snap, qi, qx, qy
 
 
+def config_of(wl, nq_total, world, scaling, th, delta, U):
+    """The ``config`` object of both arms' JSON lines (same keys)."""
+    return {
+        "workload": wl["desc"], "baseline_config": wl["baseline_idx"], "n_objects": wl["n"],
+        "n_queries": int(nq_total), "k": wl["k"], "th_quad": th, "l_max": 10,
+        "parallelism": (f"query shards x{world} ({scaling} scaling), replicated index, NCCL "
+                        f"all-gather of {'update' if delta else 'snapshot'} slices")
+        if world > 1 else "single GPU",
+        "l2": "flushed between steps (256 MB write outside the timed events); "
+              "inputs 264 MB > 126 MB L2",
+        "updates_per_tick": int(U) if delta else None,
+    }
+
+
 def run_reference(args, wl):
-    """--impl reference: the reference's CPU algorithm (C port, all host
-    threads) on a bounded sample per step, scaled to one tick."""
+    """--impl reference: the reference's CPU algorithm -- the C port of its
+    engine (oracle/, OpenMP over all host threads) -- on the same workload:
+    every step is a full steady-state tick (all queries; the index built on
+    the first tick is reused, engine.py:615-619).  Rank 0 only.  The line
+    also carries the threads=1 port figure and the unmodified Python
+    reference (baseline/_ref) timed on bounded samples."""
+    from oracle import oracle as orc
     from paper_1412_6170_b200 import synth
     from paper_1412_6170_b200.engine import resolve_th_quad
 
@@ -180,30 +257,53 @@ def run_reference(args, wl):
         return 0
     snap, qi, qx, qy = make_inputs(wl)
     th = resolve_th_quad("auto", wl["k"])
-    sample = min(len(qi), args.cpu_sample)
-    for _ in range(args.warmup):
-        cpu_port_tick_seconds(snap, qi, qx, qy, wl["k"], synth.REGION, th, min(sample, 1000))
+    index = orc.build_index(snap.x, snap.y, synth.REGION, th, 10)  # the first tick's rebuild
+    for _ in range(args.warmup):  # warm-up: the re-index and a small query batch
+        cpu_port_tick_seconds(snap, qi, qx, qy, wl["k"], synth.REGION, th, 1000, index=index)
     secs = []
     for _ in range(args.steps):
-        s, t_index, t_sample, threads = cpu_port_tick_seconds(snap, qi, qx, qy, wl["k"],
-                                                              synth.REGION, th, sample)
-        secs.append(s)
+        t = time.perf_counter()
+        orc.engine_tick(snap.ids, snap.x, snap.y, qi, qx, qy, wl["k"], synth.REGION, th,
+                        index=index)
+        secs.append(time.perf_counter() - t)
+    threads = orc.num_threads()
     ms = 1e3 * statistics.mean(secs)
     value = len(qi) / (ms / 1e3)
+    extra = {}
+    if not args.no_cpu_extras:
+        orc.set_num_threads(1)
+        s1, _, _, _ = cpu_port_tick_seconds(snap, qi, qx, qy, wl["k"], synth.REGION, th,
+                                            min(len(qi), 20_000), index=index)
+        orc.set_num_threads(threads)
+        extra["port_threads_1"] = {"value": len(qi) / s1, "unit": UNIT, "cores": 1, "kind": "port",
+                                   "sample": "steady-state tick, 20000 queries scaled"}
+        for nt in (os.cpu_count() or 1, 1):
+            r = python_reference_tick_seconds(snap, qi, qx, qy, wl["k"], synth.REGION,
+                                              2_000 if nt == 1 else 10_000, nt)
+            if r is not None:
+                extra[f"python_reference_threads_{nt}"] = r
+    orc.free_index(index)
+    delta = bool(wl.get("updates"))
+    U = int(round(wl["n"] * wl["updates"])) if delta else wl["n"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl["desc"], "n_objects": wl["n"], "n_queries": len(qi),
-                   "k": wl["k"], "th_quad": th},
+        "scaling": scaling_of(args), "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_of(wl, len(qi), args.gpus, scaling_of(args), th, delta, U),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"full index over {wl['n']} objects + {sample} of {len(qi)} "
-                                   f"queries per step, scaled to the full query count "
-                                   f"(oracle/mknn_oracle.c, OpenMP)"},
+                         "sample": f"every step a full steady-state tick: {wl['n']} objects "
+                                   f"re-indexed, all {len(qi)} queries (oracle/mknn_oracle.c, "
+                                   f"OpenMP over {threads} threads; index built once, as on the "
+                                   f"reference's non-rebuild ticks)",
+                         **({"extra": extra} if extra else {})},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def scaling_of(args) -> str:
+    return "weak" if args.scaling == "weak" else "strong"
 
 
 def main() -> int:
@@ -215,6 +315,11 @@ def main() -> int:
     ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
     ap.add_argument("--cpu-sample", type=int, default=250_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-extras", action="store_true",
+                    help="--impl reference: skip the threads=1 and Python-reference figures")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N>1: strong = the workload's queries split over the ranks "
+                         "(BASELINE configs[3]), weak = that many queries per rank")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
@@ -238,8 +343,10 @@ def main() -> int:
     k = wl["k"]
     th = resolve_th_quad("auto", k)
 
-    snap, qi, qx, qy = make_inputs(wl, world, rank)
+    strong = args.scaling == "strong"
+    snap, qi, qx, qy = make_inputs(wl, world, rank, strong)
     nq = len(qi)
+    nq_job = torch.tensor([nq], dtype=torch.int64, device=dev)
     lo, hi = (0, wl["n"])
     if world > 1:
         from paper_1412_6170_b200.sharded import ShardedEngine, shard_bounds
@@ -321,8 +428,18 @@ def main() -> int:
     t_local = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+        dist.all_reduce(nq_job)
     ms_per_step = float(t_local.item()) / args.steps
-    value = world * nq / (ms_per_step / 1e3)
+    nq_total = int(nq_job.item())
+    value = nq_total / (ms_per_step / 1e3)
+    # the replicated part (update ingest, re-index) against the
+    # query phase (index_queries + search + emission), max over ranks
+    ph = torch.tensor([statistics.mean(m.t_build_us + m.t_index_objects_us for m in tick_metrics),
+                       statistics.mean(m.t_index_queries_us + m.t_loop_us + m.t_emit_us
+                                       for m in tick_metrics)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ph, op=dist.ReduceOp.MAX)
+    replicated_us, query_phase_us = (float(v) for v in ph.tolist())
 
     # ---- e2e through the reference-facing API with pinned host buffers ----
     e2e = None
@@ -362,7 +479,7 @@ def main() -> int:
         t_e2e = torch.tensor([statistics.mean(secs)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * nq / float(t_e2e.item()), "unit": UNIT,
+        e2e = {"value": nq_total / float(t_e2e.item()), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(12 * nq + 16 * nres)}
 
     # ---- roofline of the dominant kernel (k_search) -----------------------
@@ -374,30 +491,26 @@ def main() -> int:
     t_search_s = statistics.mean(search_us) / 1e6
     search_bytes = 24 * T_records + 24 * nq + 16 * nq * k
     achieved = search_bytes / t_search_s / 1e9
-    prof = load_json(os.path.join(ROOT, "profiles", "search_kernel_traffic.json")) or {}
-    traffic = prof.get("traffic_bytes_per_launch") if prof.get("workload") == args.workload else None
+    # ncu --set full capture of the same kernel on the same workload (per launch)
+    prof = (load_json(os.path.join(ROOT, "profiles", "search_kernel_traffic.json")) or {})
+    prof = prof.get(args.workload, {}) if isinstance(prof, dict) else {}
+    traffic = prof.get("traffic_bytes_per_launch")
     tick_bytes = 24 * U + 64 * wl["n"] + 48 * nq + 24 * T_records + 16 * nq * k
     m0 = tick_metrics[-1]
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {
-            "workload": wl["desc"], "baseline_config": wl["baseline_idx"], "n_objects": wl["n"],
-            "n_queries_per_gpu": nq, "k": k, "th_quad": th, "l_max": 10,
-            "parallelism": (f"query shards x{world}, replicated index, NCCL all-gather of "
-                            f"{'update' if delta else 'snapshot'} slices") if world > 1
-                           else "single GPU",
-            "l2": "flushed between steps (256 MB write outside the timed events); "
-                  "inputs 264 MB > 126 MB L2",
-            "timed": ("Engine.update (U device-resident update records) + Engine.query_device per "
-                      "step: update apply, rebuild decision, index_objects, index_queries, search, "
-                      "emission to device CSR" if delta else
-                      "Engine.tick_device per step: rebuild decision, index_objects, "
-                      "index_queries, search, emission to device CSR"),
-            "updates_per_tick": int(U) if delta else None,
-        },
+        "scaling": scaling_of(args), "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_of(wl, nq_total, world, scaling_of(args), th, delta, U),
+        "timed": ("Engine.update (U device-resident update records) + Engine.query_device per "
+                  "step: update apply, rebuild decision, index_objects, index_queries, search, "
+                  "emission to device CSR" if delta else
+                  "Engine.tick_device per step: rebuild decision, index_objects, "
+                  "index_queries, search, emission to device CSR"),
+        "phases_max_over_ranks_us": {"replicated_reindex": replicated_us,
+                                     "query_phase": query_phase_us,
+                                     "queries_per_rank": nq},
         "e2e": e2e,
         "gpu_launches": int(launches),
         "roofline": {
@@ -428,9 +541,10 @@ def main() -> int:
             snap, qi, qx, qy, k, synth.REGION, th, min(args.cpu_sample, nq))
         line["cpu_baseline"] = {
             "value": nq / s, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"C port of the reference engine (oracle/mknn_oracle.c): full index over "
-                      f"{wl['n']} objects ({t_index:.2f} s) + {min(args.cpu_sample, nq)} of {nq} "
-                      f"queries ({t_sample - t_index:.2f} s), scaled to {nq} queries"}
+            "sample": f"C port of the reference engine (oracle/mknn_oracle.c), steady-state tick "
+                      f"(index reused): re-index of {wl['n']} objects ({t_index:.2f} s) + "
+                      f"{min(args.cpu_sample, nq)} of {nq} queries ({t_sample - t_index:.2f} s), "
+                      f"scaled to {nq} queries"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -490,6 +490,13 @@ static inline int64_t navigate_one(const or_ctx *c, int sign, int64_t *cursor,
     }
 }
 
+OR_EXPORT int or_engine_tick_ix(int64_t n, const int64_t *ids, const double *x, const double *y,
+                                int64_t nq, const int64_t *q_issuer, const double *qx,
+                                const double *qy, int k, const or_rect *r, const or_index *ix,
+                                int64_t *out_qids, int32_t *out_len, int64_t *out_nids,
+                                double *out_dist, int32_t *nav_left, int32_t *nav_right,
+                                or_metrics *met, int32_t *out_l_deep, int64_t *out_n_leaves);
+
 /* One full tick.  Outputs as or_brute_knn (padded rows in stable issuer
  * order).  nav_left/nav_right receive per-row navigate-call counts so the
  * caller can rebuild active_left/right (engine.py:661-663).  Returns 0, or
@@ -506,6 +513,21 @@ OR_EXPORT int or_engine_tick(int64_t n, const int64_t *ids, const double *x, con
      * rebuild tick */
     or_index *ix = or_build_index(nb, bx, by, r, th_quad, l_max);
     if (!ix) return -1;
+    int rc = or_engine_tick_ix(n, ids, x, y, nq, q_issuer, qx, qy, k, r, ix, out_qids, out_len,
+                               out_nids, out_dist, nav_left, nav_right, met, out_l_deep,
+                               out_n_leaves);
+    or_index_free(ix);
+    return rc;
+}
+
+/* The same tick over an index built earlier (engine.py:615-619: a tick on
+ * which should_rebuild does not fire reuses the engine's QuadIndex). */
+OR_EXPORT int or_engine_tick_ix(int64_t n, const int64_t *ids, const double *x, const double *y,
+                                int64_t nq, const int64_t *q_issuer, const double *qx,
+                                const double *qy, int k, const or_rect *r, const or_index *ix,
+                                int64_t *out_qids, int32_t *out_len, int64_t *out_nids,
+                                double *out_dist, int32_t *nav_left, int32_t *nav_right,
+                                or_metrics *met, int32_t *out_l_deep, int64_t *out_n_leaves) {
     int64_t L = ix->n_leaves;
     int64_t *s_ids = (int64_t *)malloc(sizeof(int64_t) * (n ? n : 1));
     double *s_x = (double *)malloc(sizeof(double) * (n ? n : 1));
@@ -617,8 +639,15 @@ OR_EXPORT int or_engine_tick(int64_t n, const int64_t *ids, const double *x, con
     if (out_n_leaves) *out_n_leaves = ix->n_leaves;
     free(qleaf); free(qperm); free(qorder); free(qrow);
     free(s_ids); free(s_x); free(s_y); free(cs); free(ce);
-    or_index_free(ix);
     return 0;
+}
+
+OR_EXPORT void or_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
 }
 
 OR_EXPORT int or_num_threads(void) {

@@ -64,6 +64,8 @@ def lib():
         L.or_index_free.restype = None
         L.or_index_objects.restype = ctypes.c_int64
         L.or_engine_tick.restype = ctypes.c_int
+        L.or_engine_tick_ix.restype = ctypes.c_int
+        L.or_set_num_threads.restype = None
         L.or_num_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -182,11 +184,13 @@ def free_index(index: dict) -> None:
 
 
 def engine_tick(ids, x, y, q_issuer, qx, qy, k: int, region, th_quad: int,
-                l_max: int = 10, build_xy=None) -> CSR:
+                l_max: int = 10, build_xy=None, index: dict | None = None) -> CSR:
     """engine.py:601-696 process_tick with canonical selection.
 
     The index is built from ``build_xy`` = (bx, by) -- the positions of the
-    tick that last rebuilt -- or from this tick's positions when None.
+    tick that last rebuilt -- or from this tick's positions when None; or,
+    with ``index`` (a ``build_index`` result), that index is reused as on a
+    tick where should_rebuild does not fire (engine.py:615-619).
 
     metrics holds distance_evals, pruned_leaves, clamped_objects,
     iterations_left/right and active_left/right (engine.py:88-107).
@@ -201,17 +205,20 @@ def engine_tick(ids, x, y, q_issuer, qx, qy, k: int, region, th_quad: int,
     dist = np.zeros(nq * k, np.float64)
     navl = np.zeros(nq, np.int32)
     navr = np.zeros(nq, np.int32)
-    bx, by = (x, y) if build_xy is None else (_f64(build_xy[0]), _f64(build_xy[1]))
     met = _Metrics()
     l_deep = ctypes.c_int32(0)
     n_leaves = ctypes.c_int64(0)
-    rc = lib().or_engine_tick(
-        ctypes.c_int64(n), _p(ids, _i64p), _p(x, _f64p), _p(y, _f64p), ctypes.c_int64(nq),
-        _p(q_issuer, _i64p), _p(qx, _f64p), _p(qy, _f64p), ctypes.c_int(k), ctypes.byref(r),
-        ctypes.c_int(th_quad), ctypes.c_int(l_max), _p(qids, _i64p), _p(lens, _i32p),
-        _p(nids, _i64p), _p(dist, _f64p), _p(navl, _i32p), _p(navr, _i32p),
-        ctypes.byref(met), ctypes.byref(l_deep), ctypes.byref(n_leaves),
-        ctypes.c_int64(len(bx)), _p(bx, _f64p), _p(by, _f64p))
+    head = (ctypes.c_int64(n), _p(ids, _i64p), _p(x, _f64p), _p(y, _f64p), ctypes.c_int64(nq),
+            _p(q_issuer, _i64p), _p(qx, _f64p), _p(qy, _f64p), ctypes.c_int(k), ctypes.byref(r))
+    outs = (_p(qids, _i64p), _p(lens, _i32p), _p(nids, _i64p), _p(dist, _f64p),
+            _p(navl, _i32p), _p(navr, _i32p), ctypes.byref(met), ctypes.byref(l_deep),
+            ctypes.byref(n_leaves))
+    if index is not None:
+        rc = lib().or_engine_tick_ix(*head, index["_ptr"], *outs)
+    else:
+        bx, by = (x, y) if build_xy is None else (_f64(build_xy[0]), _f64(build_xy[1]))
+        rc = lib().or_engine_tick(*head, ctypes.c_int(th_quad), ctypes.c_int(l_max), *outs,
+                                  ctypes.c_int64(len(bx)), _p(bx, _f64p), _p(by, _f64p))
     if rc != 0:
         raise ValueError(f"bad index parameters th_quad={th_quad} l_max={l_max}")
     res = _compact(qids, lens, nids, dist, k)
@@ -237,3 +244,9 @@ def active_counts(nav_calls: np.ndarray) -> list:
 
 def num_threads() -> int:
     return int(lib().or_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP threads of the port's query loop (BASELINE.md §3 asks for
+    threads=1 and threads=os.cpu_count())."""
+    lib().or_set_num_threads(ctypes.c_int(int(n)))

@@ -221,6 +221,7 @@ struct mknn_engine {
   bool q_pending = false;
   bool rows_in_host = false;   // the sliced host tick already delivered qids/len/rows
   bool retry_rebuild = false;  // false: the store's sub-cell counters may be dirty
+  bool retry_radix = false;    // the redo of a tick sorts its issuers with the radix path
   int32_t h_l_deep = 0;
   int64_t h_n_leaves = 0, h_overfull = 0, h_n_build = 0, h_n_sub = 0;
   DevStore st;
@@ -472,8 +473,10 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
     MKNN_CUDA_OK(cudaStreamWaitEvent(s, h->q_ready, 0));
     h->q_pending = false;
   }
+  const bool use_bitmap = !h->issuer_dups && !h->retry_radix;
+  h->retry_radix = false;
   if ((rc = queries_index(h->dq, h->st, h->ix, h->r, qi, qx, qy, nq, h->h_n_sub, h->issuer_bits,
-                          &bits_used, !h->issuer_dups, o.qids, h->scratch.p, s)))
+                          &bits_used, use_bitmap, o.qids, h->scratch.p, s)))
     return h->set_err(rc);
   MKNN_CUDA_OK(cudaEventRecord(h->ev[3], s));
 
@@ -623,12 +626,17 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
   if (nq) {
     // the issuer sort was planned from the previous tick's id range: if this
     // tick's range needs more bits the row order is wrong -> redo the tick
+    // dup bit 0: an issuer id repeated inside the planned range (rows by
+    // radix sort from now on); bit 1: ids beyond the planned range
     const int need = issuer_bits(mm[0], mm[1]);
     h->issuer_bits = need;
-    if (pb.dup && need <= bits_used) h->issuer_dups = true;  // a repeated issuer id
+    if (pb.dup & 1) h->issuer_dups = true;
     if (need > bits_used || pb.dup) {
       *retry = true;
       h->retry_rebuild = rebuild;
+      // the redo sorts with the radix path: ids that were out of span may
+      // still repeat, which the bitmap would only find on a third pass
+      h->retry_radix = true;
       return 0;
     }
   }

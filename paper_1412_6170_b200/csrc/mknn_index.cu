@@ -513,8 +513,12 @@ __global__ void k_issuer_rows(const uint64_t* __restrict__ keys, const uint32_t*
 // Row order without a sort when the issuers are distinct: one bit per id of
 // [min, min + 2^bits) marks the batch's ids; a query's row is the number of
 // marked ids below its own (popcount prefix over words) -- the stable issuer
-// rank of engine.py:713 when no id repeats.  A repeated id (or an id beyond
-// the planned range) raises *dup and the tick is redone with the radix sort.
+// rank of engine.py:713 when no id repeats.  A repeated id raises bit 0 of
+// *dup (the engine switches to the radix sort for good), an id beyond the
+// planned range (planned from the previous tick) raises bit 1; either way
+// the tick is redone.
+constexpr int32_t DUP_REPEATED = 1, DUP_OUT_OF_SPAN = 2;
+
 __global__ void k_issuer_mark(const long long* __restrict__ qi, int64_t nq,
                               const int64_t* __restrict__ mm, uint64_t span,
                               uint32_t* __restrict__ bm, int32_t* __restrict__ dup) {
@@ -522,11 +526,11 @@ __global__ void k_issuer_mark(const long long* __restrict__ qi, int64_t nq,
   if (i < nq) {
     const uint64_t key = (uint64_t)qi[i] - (uint64_t)mm[0];
     if (key >= span) {
-      *dup = 1;
+      atomicOr(dup, DUP_OUT_OF_SPAN);
       return;
     }
     const uint32_t bit = 1u << (key & 31);
-    if (atomicOr(&bm[key >> 5], bit) & bit) *dup = 1;
+    if (atomicOr(&bm[key >> 5], bit) & bit) atomicOr(dup, DUP_REPEATED);
   }
 }
 
@@ -542,7 +546,10 @@ __global__ void k_issuer_rank(const long long* __restrict__ qi, int64_t nq,
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < nq) {
     const uint64_t key = (uint64_t)qi[i] - (uint64_t)mm[0];
-    if (key >= span) return;  // the tick is redone (dup flag)
+    if (key >= span) {  // the tick is redone (dup flag); keep the row in bounds meanwhile
+      row[i] = 0;
+      return;
+    }
     const int64_t w = (int64_t)(key >> 5);
     const uint32_t r = (uint32_t)pre[w] + (uint32_t)__popc(bm[w] & ((1u << (key & 31)) - 1u));
     row[i] = r;

@@ -1096,11 +1096,15 @@ template <int KPL, int B, int WARPS, int MINB = 1, bool ROWS = false>
 int launch_batched(const SearchArgs& a, cudaStream_t s) {
   constexpr int N = 32 * KPL;
   const size_t smem = ROWS ? 0 : (size_t)WARPS * (B + (KPL > 1 ? 1 : 0)) * N * (sizeof(double) + sizeof(long long));
-  static bool configured = false;
-  if (!configured) {
+  // the attribute is per device: remember which devices have it
+  static unsigned long long configured = 0;  // bit d: device d
+  int dev = 0;
+  MKNN_CUDA_OK(cudaGetDevice(&dev));
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(__atomic_load_n(&configured, __ATOMIC_ACQUIRE) & bit)) {
     MKNN_CUDA_OK(cudaFuncSetAttribute(k_search<KPL, B, WARPS, MINB, ROWS>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
+    __atomic_fetch_or(&configured, bit, __ATOMIC_ACQ_REL);
   }
   const int64_t per_cta = (int64_t)WARPS * B;
   const unsigned blocks = (unsigned)((a.nq + per_cta - 1) / per_cta);

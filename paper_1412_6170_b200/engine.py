@@ -318,6 +318,10 @@ class Engine:
             self._last_build_tick = m.tick
         self.last_streamed_records = m.streamed_records
         self.last_metrics = tm
+        if self.config.self_check and m.rebuild_flag:
+            # engine.py:620-621: structural invariants of the rebuilt index
+            # (quadindex.py:51-76), AssertionError on violation
+            self.index.validate()
         return tm
 
     def _result(self, qids, lens, nids, dist, n_results, offsets=None) -> TickResult:

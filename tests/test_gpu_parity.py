@@ -492,3 +492,71 @@ def test_incremental_store_matches_full_rebuild(dist):
                         "active_left", "active_right"):
                 assert getattr(delta.last_metrics, key) == getattr(full.last_metrics, key), (t, key)
         assert delta.snapshot_size == len(ids)
+
+
+def test_self_check_validates_every_rebuilt_index(monkeypatch):
+    """engine.py:620-621: with self_check the rebuilt index is validated
+    (quadindex.py:51-76) -- on the first tick and on a should_rebuild tick;
+    a corrupted export is rejected with AssertionError."""
+    from paper_1412_6170_b200 import index as ix_mod
+
+    calls = []
+    real = ix_mod.QuadIndex.validate
+    monkeypatch.setattr(ix_mod.QuadIndex, "validate",
+                        lambda self, *a, **kw: (calls.append(self.n_leaves), real(self, *a, **kw)))
+    snap = synth.place(60_000, "uniform", seed=9)
+    with Engine(EngineConfig(k=8, region=synth.REGION, self_check=True, rebuild_window=1,
+                             rebuild_factor=1.2)) as eng:
+        for t in range(3):
+            if t == 2:  # a cluster: evaluations jump, the next tick rebuilds
+                snap.x[: 30_000] = 5000.0 + snap.x[: 30_000] * 1e-3
+                snap.y[: 30_000] = 9000.0 + snap.y[: 30_000] * 1e-3
+            qi, qx, qy = synth.queries(snap, 2000, seed=t)
+            eng.process_tick(snap.ids, snap.x, snap.y, qi, qx, qy)
+        qi, qx, qy = synth.queries(snap, 2000, seed=7)
+        eng.process_tick(snap.ids, snap.x, snap.y, qi, qx, qy)
+        assert eng.last_metrics.rebuild_flag == 1
+        assert len(calls) == 2
+        bad = eng.index
+        bad.leaf_span[0] += 1
+        with pytest.raises(AssertionError):
+            real(bad)
+
+
+def test_two_engines_large_k_in_one_process():
+    """k > 32 kernels need a >48 KB shared-memory attribute, which is per
+    device: two engines (every visible device, or the same one twice) in
+    one process both run."""
+    n_dev = torch.cuda.device_count()
+    devs = [0, 1] if n_dev > 1 else [0, 0]
+    snap = synth.place(20_000, "gaussian", seed=10, hotspots=3)
+    qi, qx, qy = synth.queries(snap, 1500, seed=10)
+    want = orc.brute_force_knn(snap.ids, snap.x, snap.y, qi, qx, qy, 128)
+    engines = [Engine(EngineConfig(k=128, region=synth.REGION, device=d)) for d in devs]
+    try:
+        for eng in engines:
+            assert_same(eng.process_tick(snap.ids, snap.x, snap.y, qi, qx, qy), want)
+    finally:
+        for eng in engines:
+            eng.close()
+
+
+def test_repeated_issuers_on_a_wider_id_range():
+    """Advisor finding: repeated issuer ids on a tick whose id range needs
+    more bits than the previous tick's (the bitmap planned from the old
+    range sees ids beyond it): the tick still comes out in stable issuer
+    order, and a later tick with a narrower range as well."""
+    rng = np.random.default_rng(31)
+    n = 4000
+    x = rng.uniform(0, 300, n)
+    y = rng.uniform(0, 300, n)
+    ids = np.arange(n, dtype=np.int64)
+    region = Rect.square(300.0)
+    with Engine(EngineConfig(k=5, region=region, th_quad=24)) as eng:
+        for t, (span, nq) in enumerate([(64, 60), (1 << 30, 900), (1 << 33, 80), (50, 300)]):
+            sel = rng.choice(n, nq, replace=False)
+            qi = rng.integers(0, span, nq).astype(np.int64)
+            qi[nq // 3: nq // 3 + 5] = qi[0]  # repeats
+            res = eng.process_tick(ids, x, y, qi, x[sel], y[sel])
+            assert_same(res, orc.brute_force_knn(ids, x, y, qi, x[sel], y[sel], 5))
+            assert eng.last_metrics.tick == t
