@@ -238,6 +238,7 @@ struct mknn_engine {
   long long* out_qids = nullptr; int64_t cap_oq = 0;
   QueryStats* stats = nullptr; int64_t cap_stats = 0;
   unsigned long long* prof = nullptr;  // MKNN_PROF=1 work counters
+  unsigned* work = nullptr;  // k_search1 batch counter
   unsigned long long* counters = nullptr;  // [0] evals [1] prunes [2] viol [3] clamped
   uint32_t* hist = nullptr;                // 2 x hist_cap
   // instrumentation buffers (config.instrument & 1)
@@ -333,6 +334,7 @@ int alloc_store(mknn_engine* h, int64_t n) {
     MKNN_CUDA_OK(cudaMalloc(&h->clamped_total, sizeof(unsigned long long)));
     h->hist_cap = (int)(ncap + 2);
     MKNN_CUDA_OK(cudaMalloc(&h->hist, sizeof(uint32_t) * 2 * h->hist_cap));
+    MKNN_CUDA_OK(cudaMalloc(&h->work, sizeof(unsigned) * 4));
   }
   if (n > h->st.cap) {
     int64_t nc = std::max<int64_t>(n, h->st.cap * 3 / 2);
@@ -503,6 +505,7 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
   a.out_dist = o.dist;
   a.n_objects = n;
   a.stats = h->stats;
+  a.work = h->work;
   a.audit = h->cfg.audit_pruning;
   {
     static const char* dp = getenv("MKNN_DEBUG_PHASE");
@@ -975,7 +978,7 @@ void mknn_destroy(mknn_engine* h) {
                   h->stats, h->counters, h->hist, h->snap_ids, h->snap_x, h->snap_y, h->ht,
                   h->winner, h->slot_of, h->d_nsnap, h->up_ids, h->up_x, h->up_y,
                   h->tk, h->tk_alt, h->tk_cnt, h->tv, h->tv_alt, h->prof, h->mark, h->moved,
-                  h->d_nmoved, h->clamped_total, h->st.kstart_alt, h->st.fill,
+                  h->d_nmoved, h->clamped_total, h->work, h->st.kstart_alt, h->st.fill,
                   h->st.qcnt, h->st.qkstart, h->st.rmflag, h->st.rm_before, h->st.mkey};
   for (void* p : ptrs)
     if (p) cudaFree(p);

@@ -239,6 +239,9 @@ struct SearchArgs {
   unsigned long long* task_keys;  // nullptr when off
   unsigned long long* task_count;
   int64_t task_cap;
+  // k_search1: persistent CTAs take query batches from *work (zeroed by
+  // search_launch before each launch)
+  unsigned* work;
 };
 
 // T from task keys: sorts keys in place (alt buffer) and sums the leaf

@@ -1011,6 +1011,547 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
   }
 }
 
+// ===== 16 < k <= 32: one-slot lists kept as store positions ===============
+//
+// Same walk as k_search (own leaf, then alternating left/right visits), but
+// between visits a query's list is kept as k store positions (4 bytes per
+// entry) in the warp's shared memory instead of (d2, id) pairs in the
+// output row: a visit gathers its query's k records back and recomputes
+// their d2 (pair_d2 is deterministic), and the emit writes each result row
+// exactly once.  The round-1 kernel wrote every row once per visit plus once
+// more in the emit (2.0x DRAM write amplification at cfg3); this one writes
+// 1.04x (ncu: 531 MB against 512 MB of rows) at the same speed.  CTAs are
+// persistent and take 32-query batches from a work counter.
+//
+// Chunk tiles in shared memory (template flag TMA, MKNN_SEARCH_VAR=1): the
+// two chunks of a step are contiguous 512-byte spans of the store, staged by
+// 1-D bulk copies (cp.async.bulk, mbarrier completion) issued one step ahead
+// into a per-warp two-slot ring, as the paper stages a cell's objects for
+// its queries.  Measured on B200 it is 3.8x slower than
+// loading the records through L1 (cfg3 search 8.95 vs 2.35 ms): a warp step
+// holds only 1 KB, and the ~160 bulk copies per 32-query batch queue on the
+// SM's copy engine (~280 cycles per request), while the L1 serves the same
+// records to the leaf's other queries.  Kept for that measurement only.
+struct L1 {
+  double d;
+  long long id;
+  int pos;  // store index of the entry (-1: empty)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, unsigned bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+constexpr int TILE = 32;  // records per ring slot: two 16-object chunks
+static_assert(chunk_for_k(32) * 2 == TILE, "a tile holds the two chunks of one step");
+
+// one step's chunks, distributed: lane l < 16 holds record l of the nearer
+// chunk, lane 16 + l record l of the other (rec = its store index, -1 when
+// the lane has none); md0 = a lower bound (float, rounded down) of the
+// nearer chunk's box min-dist2, -1 when the pick is empty
+struct Pick {
+  int rec;
+  float md0;
+};
+
+// chunk candidates of a leaf, 32 boxes at a time (lane i: chunk g + i);
+// mdf = the box min-dist2 rounded down to float (NaN once picked or past
+// the leaf: it then compares false with any kd, +inf included).  Testing mdf <= kd instead of md <= kd admits a superset of
+// the qualifying chunks (a few more scans, never fewer), so the result is
+// unchanged.
+struct ChunkIter {
+  int g, c1;
+  float mdf;
+};
+
+#define MKNN_FDEAD __int_as_float(0x7fffffff)  // NaN
+
+// the (up to) two nearest remaining chunks that qualify under kd, nearest
+// first (kd only shrinks, so a chunk that does not qualify never will)
+__device__ __forceinline__ Pick next_pick(ChunkIter& it, double kd, int ob, int oe, int c0,
+                                          const ChunkBox* __restrict__ box, double qx, double qy,
+                                          int lane) {
+  constexpr int CH = chunk_for_k(32);
+  Pick p;
+  p.rec = -1;
+  p.md0 = -1.0f;
+  for (;;) {
+    const bool cand = (double)it.mdf <= kd;  // false for NaN
+    if (!__any_sync(FULL, cand)) {
+      it.g += 32;
+      if (it.g >= it.c1) return p;
+      it.mdf = it.g + lane < it.c1 ? __double2float_rd(mindist2_box(box[it.g + lane], qx, qy)) : MKNN_FDEAD;
+      continue;
+    }
+    // nearest box first (key: mdf with the lane in the low bits; mdf >= 0,
+    // so its bits order like the values); the order only affects speed
+    unsigned key = cand ? ((__float_as_uint(it.mdf) & ~31u) | (unsigned)lane) : 0xffffffffu;
+    const unsigned k0 = __reduce_min_sync(FULL, key);
+    const int a0 = (int)(k0 & 31u);
+    if (lane == a0) {
+      it.mdf = MKNN_FDEAD;
+      key = 0xffffffffu;
+    }
+    const unsigned k1 = __reduce_min_sync(FULL, key);
+    const int a1 = k1 == 0xffffffffu ? -1 : (int)(k1 & 31u);
+    if (lane == a1) it.mdf = MKNN_FDEAD;
+    p.md0 = __uint_as_float(k0 & ~31u);
+    const int ch = lane < CH ? a0 : a1;
+    const int r = ob + (it.g - c0 + ch) * CH + (lane & (CH - 1));
+    p.rec = ch >= 0 && r < min(ob + (it.g - c0 + ch + 1) * CH, oe) ? r : -1;
+    return p;
+  }
+}
+
+// shared-memory ring of two tiles (one mbarrier each) per warp: the tiles
+// and barriers are the CTA's static shared arrays; the state is one word
+// (bits 0-1: parity of each slot's next completion, bit 2: slot to fill)
+__shared__ __align__(128) StoreRec ring_buf[2 * TILE];
+__shared__ __align__(8) unsigned long long ring_bar[2];
+
+__device__ __forceinline__ uint32_t ring_bar_addr(int s) { return smem_u32(&ring_bar[s]); }
+
+// bulk-copy one pick into the next slot (lane 0 issues); returns the slot
+__device__ __forceinline__ int ring_issue(uint32_t& R, const Pick& p, const StoreRec* __restrict__ obj,
+                                          int lane) {
+  const int s = (R >> 2) & 1;
+  R ^= 4u;
+  const unsigned v = __ballot_sync(FULL, p.rec >= 0);
+  const int s1 = __shfl_sync(FULL, p.rec, 16);
+  if (lane == 0) {
+    const unsigned n0 = __popc(v & 0xffffu), n1 = __popc(v >> 16);
+    const uint32_t bar = ring_bar_addr(s);
+    const uint32_t dst = smem_u32(&ring_buf[s * TILE]);
+    mbar_expect_tx(bar, (n0 + n1) * (unsigned)sizeof(StoreRec));
+    bulk_g2s(dst, obj + p.rec, n0 * (unsigned)sizeof(StoreRec), bar);
+    if (n1) bulk_g2s(dst + (TILE / 2) * sizeof(StoreRec), obj + s1, n1 * (unsigned)sizeof(StoreRec), bar);
+  }
+  return s;
+}
+
+__device__ __forceinline__ void ring_wait(uint32_t& R, int s) {
+  mbar_wait(ring_bar_addr(s), (R >> s) & 1u);
+  R ^= 1u << s;
+}
+
+// record `lane` of slot s: x, y, id
+__device__ __forceinline__ void ring_rec(int s, int lane, double& x, double& y, long long& id) {
+  const uint32_t a = smem_u32(&ring_buf[s * TILE + lane]);
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
+  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(id) : "r"(a + 16));
+}
+
+__device__ __forceinline__ void kth1(const L1& L, int k, double& kd, long long& ki) {
+  kd = __shfl_sync(FULL, L.d, k - 1);
+  ki = __shfl_sync(FULL, L.id, k - 1);
+}
+
+// exact (d2, id) compare-exchange carrying the store position
+__device__ __forceinline__ void cx1(double& d, long long& id, int& p, int lane, int size, int j) {
+  const double pd = __shfl_xor_sync(FULL, d, j);
+  const long long pi = __shfl_xor_sync(FULL, id, j);
+  const int pp = __shfl_xor_sync(FULL, p, j);
+  const bool asc = (lane & size) == 0;
+  const bool lower = (lane & j) == 0;
+  const bool take = (lower == asc) ? key_less(pd, pi, d, id) : key_less(d, id, pd, pi);
+  d = take ? pd : d;
+  id = take ? pi : id;
+  p = take ? pp : p;
+}
+
+__device__ __noinline__ L1 exact_sort1(L1 c, int lane) {
+  for (int size = 2; size <= 32; size <<= 1)
+    for (int j = size >> 1; j > 0; j >>= 1) cx1(c.d, c.id, c.pos, lane, size, j);
+  return c;
+}
+
+// L <- the 32 smallest of L u C (both ascending), exact networks
+__device__ __noinline__ L1 exact_merge1(L1 l, L1 c, int lane) {
+  const double rd = __shfl_xor_sync(FULL, c.d, 31);
+  const long long ri = __shfl_xor_sync(FULL, c.id, 31);
+  const int rp = __shfl_xor_sync(FULL, c.pos, 31);
+  const bool lt = key_less(rd, ri, l.d, l.id);
+  l.d = lt ? rd : l.d;
+  l.id = lt ? ri : l.id;
+  l.pos = lt ? rp : l.pos;
+  for (int j = 16; j > 0; j >>= 1) cx1(l.d, l.id, l.pos, lane, 64, j);
+  return l;
+}
+
+// insert one key into the ascending list (the last element falls off)
+__device__ __forceinline__ void insert1(L1& L, double kd, long long ki, int kp, int lane) {
+  const bool gt = key_less(kd, ki, L.d, L.id);
+  const unsigned m = __ballot_sync(FULL, gt);
+  const double ud = __shfl_up_sync(FULL, L.d, 1);
+  const long long ui = __shfl_up_sync(FULL, L.id, 1);
+  const int up = __shfl_up_sync(FULL, L.pos, 1);
+  const bool gprev = lane ? ((m >> (lane - 1)) & 1u) : false;
+  if (gt) {
+    L.d = gprev ? ud : kd;
+    L.id = gprev ? ui : ki;
+    L.pos = gprev ? up : kp;
+  }
+}
+
+// admit one batch of candidates (lane: (cd, ci, cp), (+inf, IDMAX) when it
+// does not pass; m = ballot of passing lanes): few are inserted one by one,
+// many are sorted (32-bit keys, exact fallback) and merged
+__device__ __forceinline__ void admit1(L1& L, double cd, long long ci, int cp, unsigned m, int lane,
+                                       unsigned long long* prof) {
+  const int cnt = __popc(m);
+  prof_add(prof, PROF_ADMITTED, cnt, lane);
+  prof_add(prof, cnt <= 4 ? PROF_INSERTS : PROF_SORT_MERGES, cnt <= 4 ? cnt : 1, lane);
+  if (cnt <= 4) {
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      insert1(L, __shfl_sync(FULL, cd, src), __shfl_sync(FULL, ci, src), __shfl_sync(FULL, cp, src),
+              lane);
+    }
+    return;
+  }
+  const bool empty = __shfl_sync(FULL, L.d, 0) == DINF;
+  // sort the batch
+  {
+    uint32_t key = akey(cd, 5, (uint32_t)lane);
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+      for (int j = size >> 1; j > 0; j >>= 1) {
+        const uint32_t p = __shfl_xor_sync(FULL, key, j);
+        const bool take_min = ((lane & j) == 0) == ((lane & size) == 0);
+        key = take_min ? min(key, p) : max(key, p);
+      }
+    }
+    if (akey_ties(key, 5, lane)) {
+      L1 c;
+      c.d = cd;
+      c.id = ci;
+      c.pos = cp;
+      c = exact_sort1(c, lane);
+      cd = c.d;
+      ci = c.id;
+      cp = c.pos;
+    } else {
+      const int src = (int)(key & 31u);
+      const double nd = __shfl_sync(FULL, cd, src);
+      const long long ni = __shfl_sync(FULL, ci, src);
+      const int np = __shfl_sync(FULL, cp, src);
+      cd = nd;
+      ci = ni;
+      cp = np;
+    }
+  }
+  if (empty) {  // the sorted batch is the list
+    L.d = cd;
+    L.id = ci;
+    L.pos = cp;
+    return;
+  }
+  // merge: min(A_i, B_{31-i}) holds the 32 smallest as a bitonic sequence
+  const uint32_t kl = akey(L.d, 6, (uint32_t)lane);
+  const uint32_t kc = akey(cd, 6, 32u | (uint32_t)lane);
+  const uint32_t rc = __shfl_sync(FULL, kc, 31 - lane);
+  uint32_t mm = min(kl, rc);
+  const uint32_t kept_max = __reduce_max_sync(FULL, mm);
+  const uint32_t drop_min = __reduce_min_sync(FULL, max(kl, rc));
+  const bool cut_tie = ((kept_max ^ drop_min) >> 6) == 0 && (kept_max >> 6) < (AKEY_INF >> 6);
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1) {
+    const uint32_t p = __shfl_xor_sync(FULL, mm, j);
+    mm = (lane & j) ? max(mm, p) : min(mm, p);
+  }
+  if (cut_tie || akey_ties(mm, 6, lane)) {
+    L1 c;
+    c.d = cd;
+    c.id = ci;
+    c.pos = cp;
+    L = exact_merge1(L, c, lane);
+    return;
+  }
+  const int src = (int)(mm & 31u);
+  const bool from_c = (mm & 32u) != 0;
+  const double dl = __shfl_sync(FULL, L.d, src), dc = __shfl_sync(FULL, cd, src);
+  const long long il = __shfl_sync(FULL, L.id, src), ic = __shfl_sync(FULL, ci, src);
+  const int pl = __shfl_sync(FULL, L.pos, src), pc = __shfl_sync(FULL, cp, src);
+  L.d = from_c ? dc : dl;
+  L.id = from_c ? ic : il;
+  L.pos = from_c ? pc : pl;
+}
+
+// One row of the reference's distance phase (first_iteration's own leaf,
+// engine.py:356-373, or update_nn_lists' assigned leaf, 376-393) for one
+// query: every object of the leaf except the issuer (engine.py:298-300)
+// competes; admission is (d2, id) < k-th.  Chunks whose box min-dist2
+// exceeds the k-th d2 (or the cap, see k_search1) cannot hold an admissible
+// object and are skipped.
+template <bool TMA>
+__device__ __forceinline__ void visit1(L1& L, int k, int leaf, double qx, double qy, long long me,
+                                       const SearchArgs& a, int lane, uint32_t& R, bool own,
+                                       double cap = DINF) {
+  const int ob = __ldg(&a.cell_start[leaf]), oe = __ldg(&a.cell_start[leaf + 1]);
+  const int c0 = __ldg(&a.chunk_start[leaf]), c1 = __ldg(&a.chunk_start[leaf + 1]);
+  prof_add(a.prof, own ? PROF_OWN_CHUNKS_TOTAL : PROF_EXP_CHUNKS_TOTAL, c1 - c0, lane);
+  if (!own) prof_add(a.prof, PROF_EXP_LEAF_VISITS, 1, lane);
+  double kd;
+  long long ki;
+  kth1(L, k, kd, ki);
+  if (cap < kd) {
+    kd = cap;
+    ki = IDMAX;
+  }
+  ChunkIter it;
+  it.g = c0 - 32;
+  it.c1 = c1;
+  it.mdf = MKNN_FDEAD;
+  Pick cur = next_pick(it, kd, ob, oe, c0, a.box, qx, qy, lane);
+  if (cur.md0 < 0.0f) {
+    if (!own) prof_add(a.prof, PROF_EXP_VISITS_NO_SCAN, 1, lane);
+    return;
+  }
+  int cs = TMA ? ring_issue(R, cur, a.obj, lane) : 0;
+  bool admitted = false;
+  for (;;) {
+    double x = 0.0, y = 0.0;
+    long long id = 0;
+    Pick nxt;
+    int ns = 0;
+    if constexpr (TMA) {
+      nxt = next_pick(it, kd, ob, oe, c0, a.box, qx, qy, lane);
+      if (nxt.md0 >= 0.0f) ns = ring_issue(R, nxt, a.obj, lane);
+      ring_wait(R, cs);
+      if (cur.rec >= 0) ring_rec(cs, lane, x, y, id);
+    } else {
+      if (cur.rec >= 0) {
+        const StoreRec r = ld_rec(&a.obj[cur.rec]);
+        x = r.x;
+        y = r.y;
+        id = r.id;
+      }
+    }
+    prof_add(a.prof, own ? PROF_OWN_CHUNKS_SCANNED : PROF_EXP_CHUNKS_SCANNED, 1, lane);
+    const bool valid = cur.rec >= 0;
+    const double d2 = valid ? pair_d2(qx, qy, x, y) : DINF;
+    const bool pass = valid && d2 <= kd && id != me && key_less(d2, id, kd, ki);
+    const unsigned m = __ballot_sync(FULL, pass);
+    if (m) {
+      admit1(L, pass ? d2 : DINF, pass ? id : IDMAX, pass ? cur.rec : -1, m, lane, a.prof);
+      kth1(L, k, kd, ki);
+      if (cap < kd) {
+        kd = cap;
+        ki = IDMAX;
+      }
+      admitted = true;
+    }
+    if constexpr (!TMA) nxt = next_pick(it, kd, ob, oe, c0, a.box, qx, qy, lane);
+    if (nxt.md0 < 0.0f) break;
+    cur = nxt;
+    cs = ns;
+    // the prefetch was picked before this scan tightened kd: when its
+    // nearer chunk no longer qualifies, neither does the rest of its
+    // 32-chunk group (later groups still may), so its scan is skipped
+    if ((double)nxt.md0 > kd) cur.rec = -1;
+  }
+  if (!own) prof_add(a.prof, PROF_EXP_VISITS_ADMITTING, admitted, lane);
+}
+
+// a query's list from its stored positions: gather the records, recompute d2
+__device__ __forceinline__ void list_gather(L1& L, const int32_t* __restrict__ lp, int k,
+                                            const StoreRec* __restrict__ obj, double qx, double qy,
+                                            int lane) {
+  const int p = lane < k ? lp[lane] : -1;
+  L.pos = p;
+  L.d = DINF;
+  L.id = IDMAX;
+  if (p >= 0) {
+    const StoreRec r = ld_rec(&obj[p]);
+    L.d = pair_d2(qx, qy, r.x, r.y);
+    L.id = r.id;
+  }
+}
+
+template <int B, int MINB, bool TMA>
+__global__ void __launch_bounds__(32, MINB) k_search1(const __grid_constant__ SearchArgs a) {
+  static_assert(B <= 32, "one query per lane");
+  __shared__ double2 cw_tab[MAX_L_MAX + 1];
+  __shared__ int32_t lists[B * 32];  // the batch's lists as store positions
+  const int lane = threadIdx.x;
+  const int l_deep = __ldg(&a.scalars[0]);
+  if (lane <= l_deep)
+    cw_tab[lane] = make_double2(__dmul_rn(a.r.w, pow2_neg(lane)), __dmul_rn(a.r.h, pow2_neg(lane)));
+  uint32_t R = 0;
+  if (lane == 0) {
+    mbar_init(ring_bar_addr(0), 1);
+    mbar_init(ring_bar_addr(1), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const bool cw_exact =
+      (a.r.w == 0.0 || a.r.w >= 0x1p-1000) && (a.r.h == 0.0 || a.r.h >= 0x1p-1000);
+  const double2* cw = cw_exact ? cw_tab : nullptr;
+  const int k = a.k;
+
+  for (;;) {
+    unsigned batch = 0;
+    if (lane == 0) batch = atomicAdd(a.work, 1u);
+    batch = __shfl_sync(FULL, batch, 0);
+    if ((int64_t)batch * B >= a.nq) break;
+    const int t0 = (int)batch * B;  // queries < 2^31 (uint32 orders)
+    const int nb = (int)((a.nq - t0) < B ? (a.nq - t0) : B);
+
+    // per-lane query state (lane q < nb owns query t0 + q)
+    const bool mine = lane < nb;
+    uint32_t own = 0, qrow = 0;
+    double qx = 0.0, qy = 0.0, thr = DINF;
+    long long me = 0;
+    int cur_l = -1, cur_r = 0;
+    uint32_t evals = 0, prunes = 0, viol = 0, calls_l = 0, calls_r = 0;
+    bool act_l = false, act_r = false;
+    if (mine) {
+      const uint32_t q = __ldg(&a.q_order[t0 + lane]);
+      qrow = __ldg(&a.q_row[q]);
+      qx = __ldg(&a.qx[q]);
+      qy = __ldg(&a.qy[q]);
+      me = __ldg(&a.qi[q]);
+      own = __ldg(&a.q_leaf[q]);
+      cur_l = (int)__ldg(&a.leaf_key[own]) - 1;
+      cur_r = (int)(__ldg(&a.leaf_key[own]) + __ldg(&a.leaf_span[own]));
+      act_l = act_r = true;
+      const int pop = __ldg(&a.cell_start[own + 1]) - __ldg(&a.cell_start[own]);
+      evals = (uint32_t)pop;  // first_iteration row (rows with 0 candidates dropped, engine.py:334-338)
+      if (pop > 0) emit_task(a, 0, 0, own);
+    }
+
+    // first_iteration: every query against its own leaf, with the previous
+    // query's own-pass k-th distance as a cap when both share the leaf and
+    // its list excludes this issuer (see k_search: d <= d_prev(k) + |q -
+    // q_prev|, padded by 2^-30 relative; the list after the pass -- and the
+    // navigation threshold taken from it, engine.py:415 -- is unchanged)
+    bool excl = false;  // the previous query's list excludes this query's issuer
+    for (int j = 0; j < nb; j++) {
+      const double jx = __shfl_sync(FULL, qx, j), jy = __shfl_sync(FULL, qy, j);
+      const long long jme = __shfl_sync(FULL, me, j);
+      const uint32_t jown = __shfl_sync(FULL, own, j);
+      // previous query's coordinates, leaf and own-pass k-th d2 (thr)
+      const int jp = j > 0 ? j - 1 : 0;
+      const double p_x = __shfl_sync(FULL, qx, jp), p_y = __shfl_sync(FULL, qy, jp);
+      const double p_kd = __shfl_sync(FULL, thr, jp);
+      const uint32_t p_own = __shfl_sync(FULL, own, jp);
+      double cap = DINF;
+      if (j > 0 && jown == p_own && p_kd < DINF && excl) {
+        const double dx = jx - p_x, dy = jy - p_y;
+        const double rr = sqrt(p_kd) + sqrt(dx * dx + dy * dy);
+        cap = rr * rr * (1.0 + 0x1p-30) + 0x1p-1000;
+      }
+      L1 L;
+      L.d = DINF;
+      L.id = IDMAX;
+      L.pos = -1;
+      visit1<TMA>(L, k, (int)jown, jx, jy, jme, a, lane, R, true, cap);
+      double kd;
+      long long ki;
+      kth1(L, k, kd, ki);
+      if (lane == j) thr = kd;
+      const long long nme = __shfl_sync(FULL, me, j + 1 < 32 ? j + 1 : j);
+      excl = !__any_sync(FULL, L.id == nme);
+      lists[j * 32 + lane] = lane < k ? L.pos : -1;
+    }
+
+    // direction loop, left first (engine.py:645-681)
+    bool go_right = false;
+    if (a.debug_phase == 1) act_l = act_r = false;
+    while (__any_sync(FULL, act_l || act_r)) {
+      const bool act = go_right ? act_r : act_l;
+      int li = -1;
+      if (act) {
+        int cur = go_right ? cur_r : cur_l;
+        li = navigate(a, l_deep, go_right ? 1 : 0, cur, thr, qx, qy, me, prunes, viol, cw);
+        if (go_right) {
+          calls_r++;
+          cur_r = cur;
+          act_r = li >= 0;
+        } else {
+          calls_l++;
+          cur_l = cur;
+          act_l = li >= 0;
+        }
+        if (li >= 0) {
+          emit_task(a, go_right ? 2 : 1, (go_right ? calls_r : calls_l) - 1, li);
+          evals += (uint32_t)(__ldg(&a.cell_start[li + 1]) - __ldg(&a.cell_start[li]));
+        }
+      }
+      // update_nn_lists: merge each assigned leaf into its query's list
+      unsigned pend = __ballot_sync(FULL, li >= 0);
+      while (pend) {
+        const int j = __ffs(pend) - 1;
+        pend &= pend - 1;
+        const int jl = __shfl_sync(FULL, li, j);
+        const double jx = __shfl_sync(FULL, qx, j), jy = __shfl_sync(FULL, qy, j);
+        const long long jme = __shfl_sync(FULL, me, j);
+        L1 L;
+        list_gather(L, lists + j * 32, k, a.obj, jx, jy, lane);
+        visit1<TMA>(L, k, jl, jx, jy, jme, a, lane, R, false);
+        lists[j * 32 + lane] = lane < k ? L.pos : -1;
+        double kd;
+        long long ki;
+        kth1(L, k, kd, ki);
+        if (lane == j) thr = kd;
+      }
+      __syncwarp();
+      go_right = !go_right;
+    }
+
+    // _emit: canonical order already; sqrt correctly rounded (engine.py:706);
+    // every result row is written once (streaming stores)
+#pragma unroll 2
+    for (int j = 0; j < nb; j++) {
+      const uint32_t row = __shfl_sync(FULL, qrow, j);
+      const double jx = __shfl_sync(FULL, qx, j), jy = __shfl_sync(FULL, qy, j);
+      const int p = lane < k ? lists[j * 32 + lane] : -1;
+      const bool ok = p >= 0;
+      if (ok) {
+        const StoreRec r = ld_rec(&a.obj[p]);
+        __stcs(&a.out_nids[(int64_t)row * k + lane], r.id);
+        __stcs(&a.out_dist[(int64_t)row * k + lane], __dsqrt_rn(pair_d2(jx, jy, r.x, r.y)));
+      }
+      const int len = __popc(__ballot_sync(FULL, ok));
+      if (lane == 0) a.out_len[row] = len;
+    }
+    if (mine) {
+      QueryStats st;
+      st.evals = evals;
+      st.prunes = prunes;
+      st.nav_left = (uint16_t)min(calls_l, 65535u);
+      st.nav_right = (uint16_t)min(calls_r, 65535u);
+      st.violations = viol;
+      a.stats[t0 + lane] = st;
+    }
+    __syncwarp();
+  }
+}
+
 constexpr int HIST_SMEM = 1024;
 
 // one histogram count; lanes holding the same value (most queries make the
@@ -1113,8 +1654,53 @@ int launch_batched(const SearchArgs& a, cudaStream_t s) {
   return 0;
 }
 
+// resident CTAs of k_search1 per SM (1-warp CTAs; registers bound it)
+constexpr int SEARCH1_CTAS_PER_SM = 32;
+
+template <int B, bool TMA>
+int launch_search1(const SearchArgs& a, cudaStream_t s) {
+  int dev = 0;
+  MKNN_CUDA_OK(cudaGetDevice(&dev));
+  int sms = 0;
+  MKNN_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t batches = (a.nq + B - 1) / B;
+  int64_t grid = std::min<int64_t>(batches, (int64_t)sms * SEARCH1_CTAS_PER_SM);
+  MKNN_CUDA_OK(cudaMemsetAsync(a.work, 0, sizeof(unsigned), s));
+  MKNN_LAUNCH k_search1<B, SEARCH1_CTAS_PER_SM, TMA><<<(unsigned)grid, 32, 0, s>>>(a);
+  MKNN_CUDA_OK(cudaGetLastError());
+  return 0;
+}
+
 int search_launch(const SearchArgs& a, cudaStream_t s) {
   if (a.nq == 0) return 0;
+  // MKNN_SEARCH_V0=1: the round-1 kernel (lists in the output rows, record
+  // loads through L1) for A/B measurements
+  static const bool v0 = [] {
+    const char* e = getenv("MKNN_SEARCH_V0");
+    return e && e[0] == '1';
+  }();
+  // 16 < k <= 32: k_search1 (lists as positions in shared memory, rows
+  // written once); k <= 16: the row-resident kernel, measured 3-11 % faster
+  // there (the per-visit position gather weighs more on short lists)
+  if (a.k > 16 && a.k <= 32 && !v0) {
+    const double qd = (double)a.nq / (double)(a.n_objects > 0 ? a.n_objects : 1);
+    // MKNN_SEARCH_VAR=1: the chunk-tile ring filled by bulk copies (TMA), an
+    // experiment kept for measurement (3.8x slower)
+    static const bool ring = [] {
+      const char* e = getenv("MKNN_SEARCH_VAR");
+      return e && e[0] == '1';
+    }();
+    if (ring) {
+      if (qd < 0.015) return launch_search1<4, true>(a, s);
+      if (qd < 0.04) return launch_search1<8, true>(a, s);
+      if (qd < 0.06) return launch_search1<16, true>(a, s);
+      return launch_search1<32, true>(a, s);
+    }
+    if (qd < 0.015) return launch_search1<4, false>(a, s);
+    if (qd < 0.04) return launch_search1<8, false>(a, s);
+    if (qd < 0.06) return launch_search1<16, false>(a, s);
+    return launch_search1<32, false>(a, s);
+  }
   // k <= 32: lists in the output rows (no shared memory: L1 holds the leaf
   // records and boxes), 32 queries per warp (every lane navigates), one
   // warp per CTA (a finished warp frees its slot at once), <= 64 registers:
