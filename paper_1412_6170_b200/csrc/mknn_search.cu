@@ -489,23 +489,175 @@ __device__ __forceinline__ bool akey64_ties(const unsigned long long (&kk)[KPL],
 }
 
 // bitonic sort of the first S slots (32 * S keys) of kk
-template <int KPL, int S>
-__device__ __forceinline__ void sort_prefix(unsigned long long (&kk)[KPL], int lane) {
+template <int KPL, int S, typename KT>
+__device__ __forceinline__ void sort_prefix(KT (&kk)[KPL], int lane) {
 #pragma unroll
   for (int size = 2; size <= 32 * S; size <<= 1) {
 #pragma unroll
-    for (int j = size >> 1; j > 0; j >>= 1) step_key<KPL, unsigned long long, S>(kk, lane, size, j);
+    for (int j = size >> 1; j > 0; j >>= 1) step_key<KPL, KT, S>(kk, lane, size, j);
   }
 }
 
 // a partial flush (nbuf <= 32, one slot) sorts one slot; otherwise all
 // (intermediate widths measured slower: code size)
-template <int KPL>
-__device__ __forceinline__ void sort_used_slots(unsigned long long (&kk)[KPL], int nbuf, int lane) {
+template <int KPL, typename KT>
+__device__ __forceinline__ void sort_used_slots(KT (&kk)[KPL], int nbuf, int lane) {
   if (KPL > 1 && KPL <= 4 && nbuf <= 32)
     sort_prefix<KPL, 1>(kk, lane);
   else
     sort_prefix<KPL, KPL>(kk, lane);
+}
+
+// neighbours (element e, e + 1) of a KPL-slot 32-bit key sequence with
+// equal truncated keys (other than +inf sentinels)?
+template <int KPL>
+__device__ __forceinline__ bool akey32_ties(const uint32_t (&kk)[KPL], int bits, int lane) {
+  bool tie = false;
+#pragma unroll
+  for (int s = 0; s < KPL; s++) {
+    const uint32_t dn = __shfl_down_sync(FULL, kk[s], 1);
+    const uint32_t nx = (s + 1 < KPL) ? __shfl_sync(FULL, kk[s + 1 < KPL ? s + 1 : s], 0) : ~0u;
+    const uint32_t nk = lane < 31 ? dn : nx;
+    tie |= ((kk[s] ^ nk) >> bits) == 0 && (kk[s] >> bits) < (AKEY_INF >> bits) &&
+           !(s + 1 == KPL && lane == 31);
+  }
+  return __any_sync(FULL, tie);
+}
+
+// exact (d2, id) fallback of merge_buffer (equal truncated keys)
+template <int KPL>
+__device__ __noinline__ void merge_buffer_exact(List<KPL>& L, const double* bufd,
+                                                const long long* bufi, int nbuf, int lane) {
+  double cd[KPL];
+  long long ci[KPL];
+#pragma unroll
+  for (int s = 0; s < KPL; s++) {
+    const int e = (s << 5) | lane;
+    cd[s] = e < nbuf ? bufd[e] : DINF;
+    ci[s] = e < nbuf ? bufi[e] : IDMAX;
+  }
+  bitonic_sort<KPL>(cd, ci, lane);
+  bitonic_merge_into<KPL>(L, cd, ci, lane);
+  __syncwarp();
+}
+
+// Odd-even transposition on the exact (d2, id) order until sorted.  The
+// input is already sorted by truncated key, so only runs of equal truncated
+// keys can be out of order; each round fixes pairs inside them (typically
+// one or two rounds).
+template <int KPL>
+__device__ __forceinline__ void repair_runs(List<KPL>& L, int lane) {
+  for (;;) {
+    bool sw = false;
+    // pairs (2i, 2i + 1): lanes (even, odd) of every slot
+#pragma unroll
+    for (int s = 0; s < KPL; s++) {
+      const double pd = __shfl_xor_sync(FULL, L.d[s], 1);
+      const long long pi = __shfl_xor_sync(FULL, L.id[s], 1);
+      const bool bad = (lane & 1) ? key_less(L.d[s], L.id[s], pd, pi) : key_less(pd, pi, L.d[s], L.id[s]);
+      L.d[s] = bad ? pd : L.d[s];
+      L.id[s] = bad ? pi : L.id[s];
+      sw |= bad;
+    }
+    // pairs (2i + 1, 2i + 2): lanes (odd, even) inside a slot, and lane 31
+    // of slot s with lane 0 of slot s + 1
+    double nd[KPL];
+    long long ni[KPL];
+#pragma unroll
+    for (int s = 0; s < KPL; s++) {
+      const double dn = __shfl_down_sync(FULL, L.d[s], 1), up = __shfl_up_sync(FULL, L.d[s], 1);
+      const long long idn = __shfl_down_sync(FULL, L.id[s], 1), iup = __shfl_up_sync(FULL, L.id[s], 1);
+      const double nx = __shfl_sync(FULL, L.d[s + 1 < KPL ? s + 1 : s], 0);
+      const long long inx = __shfl_sync(FULL, L.id[s + 1 < KPL ? s + 1 : s], 0);
+      const double pv = __shfl_sync(FULL, L.d[s > 0 ? s - 1 : 0], 31);
+      const long long ipv = __shfl_sync(FULL, L.id[s > 0 ? s - 1 : 0], 31);
+      nd[s] = L.d[s];
+      ni[s] = L.id[s];
+      if (lane & 1) {  // left element of its pair: partner is the next element
+        const bool has = lane < 31 || s + 1 < KPL;
+        const double od = lane < 31 ? dn : nx;
+        const long long oi = lane < 31 ? idn : inx;
+        if (has && key_less(od, oi, L.d[s], L.id[s])) {
+          nd[s] = od;
+          ni[s] = oi;
+          sw = true;
+        }
+      } else {  // right element: partner is the previous element
+        const bool has = lane > 0 || s > 0;
+        const double od = lane > 0 ? up : pv;
+        const long long oi = lane > 0 ? iup : ipv;
+        if (has && key_less(L.d[s], L.id[s], od, oi)) {
+          nd[s] = od;
+          ni[s] = oi;
+        }
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < KPL; s++) {
+      L.d[s] = nd[s];
+      L.id[s] = ni[s];
+    }
+    if (!__any_sync(FULL, sw)) return;
+  }
+}
+
+// L <- the N smallest of L u buffer[0, nbuf); L ascending.  The networks
+// move 32-bit keys (akey: d2 as float rounded down, source index in the low
+// SB bits); runs of equal truncated keys are put in exact (d2, id) order
+// afterwards (repair_runs), and equal truncated keys across the cut between
+// the kept and the dropped halves send the merge to the exact networks.  rowd/rowi: the list's
+// shared-memory home (overwritten), bufd/bufi: the buffer.
+template <int KPL>
+__device__ __forceinline__ void merge_buffer32(List<KPL>& L, const double* bufd,
+                                               const long long* bufi, int nbuf, double* rowd,
+                                               long long* rowi, int lane) {
+  constexpr int N = 32 * KPL;
+  constexpr int SB = KPL <= 2 ? 7 : (KPL <= 4 ? 8 : (KPL <= 8 ? 9 : 10));  // bits for 2N sources
+  uint32_t kb[KPL], m[KPL];
+#pragma unroll
+  for (int s = 0; s < KPL; s++) {
+    const int e = (s << 5) | lane;
+    kb[s] = e < nbuf ? akey(bufd[e], SB, (uint32_t)(N + e)) : (~0u << SB) | (uint32_t)(N + e);
+    rowd[e] = L.d[s];
+    rowi[e] = L.id[s];
+  }
+  sort_used_slots<KPL>(kb, nbuf, lane);
+  uint32_t kept_max = 0, drop_min = ~0u;
+#pragma unroll
+  for (int s = 0; s < KPL; s++) {
+    const uint32_t kl = akey(L.d[s], SB, (uint32_t)((s << 5) | lane));
+    const uint32_t rb = __shfl_sync(FULL, kb[KPL - 1 - s], 31 - lane);
+    m[s] = min(kl, rb);
+    kept_max = max(kept_max, m[s]);
+    drop_min = min(drop_min, max(kl, rb));
+  }
+  kept_max = __reduce_max_sync(FULL, kept_max);
+  drop_min = __reduce_min_sync(FULL, drop_min);
+  const bool cut_tie = ((kept_max ^ drop_min) >> SB) == 0 && (kept_max >> SB) < (AKEY_INF >> SB);
+#pragma unroll
+  for (int j = N >> 1; j > 0; j >>= 1) step_key<KPL>(m, lane, N, j);
+  __syncwarp();
+  if (cut_tie) {
+    merge_buffer_exact<KPL>(L, bufd, bufi, nbuf, lane);
+    return;
+  }
+  // k <= 64 (16 key bits): truncated ties are rare, the exact networks
+  // take them; k <= 128 (15 bits over twice the keys): ~2 near-ties per
+  // merge, repaired in place
+  const bool ties = akey32_ties<KPL>(m, SB, lane);
+  if (KPL < 4 && ties) {
+    merge_buffer_exact<KPL>(L, bufd, bufi, nbuf, lane);
+    return;
+  }
+#pragma unroll
+  for (int s = 0; s < KPL; s++) {
+    const int src = (int)(m[s] & ((1u << SB) - 1u));
+    const bool from_list = src < N, pad = src - N >= nbuf;  // pad: an unused buffer slot
+    L.d[s] = from_list ? rowd[src] : (pad ? DINF : bufd[src - N]);
+    L.id[s] = from_list ? rowi[src] : (pad ? IDMAX : bufi[src - N]);
+  }
+  __syncwarp();
+  if (KPL >= 4 && ties) repair_runs<KPL>(L, lane);
 }
 
 // L <- the N smallest of L u buffer[0, nbuf); L ascending.  rowd/rowi: the
@@ -571,6 +723,19 @@ __device__ __noinline__ void merge_buffer(List<KPL>& L, const double* bufd, cons
   __syncwarp();
 }
 
+// KPL <= 4 (k <= 128): 32-bit keys (>= 15 mantissa bits); wider lists merge
+// 64-bit keys (with 14 bits or fewer, truncated ties at the cut become
+// frequent enough to lose: k = 256 measured 56 -> 63 ms)
+template <int KPL>
+__device__ __forceinline__ void merge_buffer_k(List<KPL>& L, const double* bufd,
+                                               const long long* bufi, int nbuf, double* rowd,
+                                               long long* rowi, int lane) {
+  if constexpr (KPL <= 4)
+    merge_buffer32<KPL>(L, bufd, bufi, nbuf, rowd, rowi, lane);
+  else
+    merge_buffer<KPL>(L, bufd, bufi, nbuf, rowd, rowi, lane);
+}
+
 template <int KPL>
 __device__ __forceinline__ void visit_leaf_buf(List<KPL>& L, int k, int leaf, double qx, double qy,
                                                long long me, const SearchArgs& a, int lane,
@@ -614,7 +779,7 @@ __device__ __forceinline__ void visit_leaf_buf(List<KPL>& L, int k, int leaf, do
         __syncwarp();
         if (nbuf > N - 32) {
           prof_add(a.prof, PROF_SORT_MERGES, 1, lane);
-          merge_buffer<KPL>(L, bufd, bufi, nbuf, rowd, rowi, lane);
+          merge_buffer_k<KPL>(L, bufd, bufi, nbuf, rowd, rowi, lane);
           nbuf = 0;
           list_kth<KPL>(L, k, kd, ki);
         }
@@ -623,7 +788,7 @@ __device__ __forceinline__ void visit_leaf_buf(List<KPL>& L, int k, int leaf, do
   }
   if (nbuf) {
     prof_add(a.prof, PROF_INSERTS, 1, lane);  // (k > 32: counts final partial merges)
-    merge_buffer<KPL>(L, bufd, bufi, nbuf, rowd, rowi, lane);
+    merge_buffer_k<KPL>(L, bufd, bufi, nbuf, rowd, rowi, lane);
   }
 }
 
@@ -1717,9 +1882,11 @@ int search_launch(const SearchArgs& a, cudaStream_t s) {
   if (a.k <= 32) return launch_batched<1, 32, 1, 32, true>(a, s);
   // k > 32: the per-warp lists (B * 16 * k bytes of shared memory) bound the
   // resident warps, so fewer queries per warp win (measured at cfg3 objects:
-  // k = 64 / 128 / 256 / 512 -24 / -18 / -24 / -17 % against 16/8/4/2)
+  // k = 64 / 128 / 256 / 512 -24 / -18 / -24 / -17 % against 16/8/4/2; k =
+  // 128 with 32-bit merge keys: 2 queries per warp 12.6 ms, 1: 13.5, 4:
+  // 13.0, 8: 16.0)
   if (a.k <= 64) return launch_batched<2, 8, 4>(a, s);
-  if (a.k <= 128) return launch_batched<4, 4, 16>(a, s);
+  if (a.k <= 128) return launch_batched<4, 2, 16>(a, s);
   if (a.k <= 256) return launch_batched<8, 1, 8>(a, s);
   if (a.k <= 512) return launch_batched<16, 1, 4>(a, s);
   return fail_msg(E_UNSUPPORTED, "k > 512 is not supported by the device top-k");

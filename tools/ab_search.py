@@ -12,17 +12,19 @@ snap = synth.place(n, dist, seed=3)
 qi, qx, qy = synth.queries(snap, nq, seed=3)
 dev = torch.device("cuda:0")
 d = [torch.as_tensor(a, device=dev) for a in (snap.ids, snap.x, snap.y, qi, qx, qy)]
-ts = []
+ts, ti = [], []
 with Engine(EngineConfig(k=k, region=synth.REGION)) as eng:
     out = None
     for it in range(iters):
         out = eng.tick_device(*d, out=out)
         torch.cuda.synchronize()
         ts.append(eng.last_metrics.t_loop_us)
+        ti.append(eng.last_metrics.t_index_objects_us)
     m = eng.last_metrics
     h = hashlib.sha256()
     for key in ("query_ids", "lengths", "offsets", "neighbour_ids", "distances"):
         h.update(out[key].cpu().numpy().tobytes())
 tag = "v0" if os.environ.get("MKNN_SEARCH_V0") == "1" else "v1"
-print(f"{tag} {dist} n={n} nq={nq} k={k}: search us {sorted(ts)[len(ts)//2]} (all {ts}) "
+tag += os.environ.get("AB_TAG", "")
+print(f"{tag} {dist} n={n} nq={nq} k={k}: search us {sorted(ts)[len(ts)//2]} idx_obj us {sorted(ti)[len(ti)//2]} (all {ts}) "
       f"evals {m.distance_evals} prunes {m.pruned_leaves} digest {h.hexdigest()[:16]}", flush=True)
