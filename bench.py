@@ -336,10 +336,18 @@ def main() -> int:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # MKNN_BENCH_BACKEND=gloo: every rank on cuda:0 with gloo collectives (a
+    # functional check of the N > 1 path on a one-GPU box; never a bench value)
+    backend = os.environ.get("MKNN_BENCH_BACKEND", "nccl")
+    if backend == "gloo":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     k = wl["k"]
     th = resolve_th_quad("auto", k)
 
@@ -373,9 +381,9 @@ def main() -> int:
         ulo, uhi = shard_bounds(U, world, rank) if world > 1 else (0, U)
         d_up = [(T(b[0][ulo:uhi]), T(b[1][ulo:uhi]), T(b[2][ulo:uhi])) for b in batches]
         if world > 1:
-            eng.load_slices(T(snap.ids[lo:hi]), T(snap.x[lo:hi]), T(snap.y[lo:hi]))
+            eng.load_slices(T(snap.ids[lo:hi]), T(snap.x[lo:hi]), T(snap.y[lo:hi]), n_total=wl["n"])
             step = lambda out, i: eng.update_tick_device(*d_up[i % n_batches], d_qi, d_qx, d_qy,  # noqa: E731
-                                                         out=out)
+                                                         out=out, n_total=U)
         else:
             engine.load(snap.ids, snap.x, snap.y)
 
@@ -386,7 +394,8 @@ def main() -> int:
         U = wl["n"]
         d_ids, d_x, d_y = T(snap.ids[lo:hi]), T(snap.x[lo:hi]), T(snap.y[lo:hi])
         if world > 1:
-            step = lambda out, i: eng.tick_device(d_ids, d_x, d_y, d_qi, d_qx, d_qy, out=out)  # noqa: E731
+            step = lambda out, i: eng.tick_device(d_ids, d_x, d_y, d_qi, d_qx, d_qy, out=out,  # noqa: E731
+                                                  n_total=wl["n"])
         else:
             step = lambda out, i: engine.tick_device(d_ids, d_x, d_y, d_qi, d_qx, d_qy, out=out)  # noqa: E731
     out = engine.alloc_device_out(nq, dev)
@@ -458,14 +467,14 @@ def main() -> int:
                     engine.update(*h_up[i % n_batches])
                     return engine.query(*h_q, out=h_out)
             else:
-                e2e_step = lambda i: eng.update_tick(*h_up[i % n_batches], *h_q)  # noqa: E731
+                e2e_step = lambda i: eng.update_tick(*h_up[i % n_batches], *h_q, n_total=U)  # noqa: E731
             h2d = 24 * (uhi - ulo) + 24 * nq
         else:
             h_snap = [pin(snap.ids[lo:hi]), pin(snap.x[lo:hi]), pin(snap.y[lo:hi])]
             if world == 1:
                 e2e_step = lambda i: engine.process_tick(*h_snap, *h_q, out=h_out)  # noqa: E731
             else:
-                e2e_step = lambda i: eng.process_tick(*h_snap, *h_q)  # noqa: E731
+                e2e_step = lambda i: eng.process_tick(*h_snap, *h_q, n_total=wl["n"])  # noqa: E731
             h2d = 24 * (hi - lo) + 24 * nq
         e2e_step(0)  # warm the host path
         if world > 1:

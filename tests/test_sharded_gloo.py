@@ -18,7 +18,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1412_6170_b200.sharded import all_gather_columns, shard_bounds, shard_queries
+from paper_1412_6170_b200.sharded import all_gather_records, shard_bounds, shard_queries
 
 
 def _free_port() -> int:
@@ -57,7 +57,12 @@ def _worker(rank, world, port, n, nq, k, ret):
         lo, hi = shard_bounds(n, world, rank)
         cols = [torch.from_numpy(snap.ids[lo:hi].copy()), torch.from_numpy(snap.x[lo:hi].copy()),
                 torch.from_numpy(snap.y[lo:hi].copy())]
-        ids, x, y = all_gather_columns(cols)
+        # sizes known from shard_bounds (no exchange) and exchanged: same records
+        ids, x, y = all_gather_records(*cols, n_total=n)
+        ids2, x2, y2 = all_gather_records(*cols)
+        assert torch.equal(ids, ids2) and torch.equal(x, x2) and torch.equal(y, y2)
+        with pytest.raises(ValueError):
+            all_gather_records(*cols, n_total=n + 2 * world + 1)
         sel = shard_queries(qi, world, rank)
         res = orc.brute_force_knn(ids.numpy(), x.numpy(), y.numpy(), qi[sel], qx[sel], qy[sel], k)
         evals = torch.tensor([int(res.lengths.sum())], dtype=torch.int64)
@@ -109,9 +114,9 @@ def _delta_worker(rank, world, port, n, nq, k, ret):
         for tick in range(2):
             uid, ux, uy = synth.updates(snap, 0.1, tick, seed=5)
             lo, hi = shard_bounds(len(uid), world, rank)
-            g_id, g_x, g_y = all_gather_columns([torch.from_numpy(uid[lo:hi].copy()),
-                                                 torch.from_numpy(ux[lo:hi].copy()),
-                                                 torch.from_numpy(uy[lo:hi].copy())])
+            g_id, g_x, g_y = all_gather_records(torch.from_numpy(uid[lo:hi].copy()),
+                                                torch.from_numpy(ux[lo:hi].copy()),
+                                                torch.from_numpy(uy[lo:hi].copy()), n_total=len(uid))
             assert np.array_equal(g_id.numpy(), uid)
             synth.apply_updates(snap, g_id.numpy(), g_x.numpy(), g_y.numpy())
             qi, qx, qy = synth.queries(snap, nq, seed=tick)
