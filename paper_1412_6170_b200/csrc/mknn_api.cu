@@ -237,6 +237,7 @@ struct mknn_engine {
   int64_t* offsets = nullptr; int64_t cap_off = 0;
   long long* out_qids = nullptr; int64_t cap_oq = 0;
   QueryStats* stats = nullptr; int64_t cap_stats = 0;
+  int32_t* own_pos = nullptr; double* own_thr = nullptr; int64_t cap_own = 0;  // k_own1 -> k_search1
   unsigned long long* prof = nullptr;  // MKNN_PROF=1 work counters
   unsigned* work = nullptr;  // k_search1 batch counter
   unsigned long long* counters = nullptr;  // [0] evals [1] prunes [2] viol [3] clamped
@@ -406,6 +407,13 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
   if ((rc = alloc_store(h, std::max<int64_t>(n, 1)))) return h->set_err(rc);
   if ((rc = alloc_queries(h, std::max<int64_t>(nq, 1)))) return h->set_err(rc);
   if ((rc = grow(h->stats, h->cap_stats, std::max<int64_t>(nq, 1)))) return h->set_err(rc);
+  if (k > 16 && k <= 32 && nq > h->cap_own) {
+    int64_t c = h->cap_own;
+    if ((rc = grow(h->own_thr, c, nq))) return h->set_err(rc);
+    c = h->cap_own * 32;
+    if ((rc = grow(h->own_pos, c, nq * 32))) return h->set_err(rc);
+    h->cap_own = c / 32;
+  }
   const int64_t rows = std::max<int64_t>(nq * (int64_t)k, 1);
   if (rows > h->cap_rows) {
     int64_t c = h->cap_rows;
@@ -506,6 +514,8 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
   a.n_objects = n;
   a.stats = h->stats;
   a.work = h->work;
+  a.own_pos = h->own_pos;
+  a.own_thr = h->own_thr;
   a.audit = h->cfg.audit_pruning;
   {
     static const char* dp = getenv("MKNN_DEBUG_PHASE");
@@ -979,7 +989,8 @@ void mknn_destroy(mknn_engine* h) {
                   h->winner, h->slot_of, h->d_nsnap, h->up_ids, h->up_x, h->up_y,
                   h->tk, h->tk_alt, h->tk_cnt, h->tv, h->tv_alt, h->prof, h->mark, h->moved,
                   h->d_nmoved, h->clamped_total, h->work, h->st.kstart_alt, h->st.fill,
-                  h->st.qcnt, h->st.qkstart, h->st.rmflag, h->st.rm_before, h->st.mkey};
+                  h->st.qcnt, h->st.qkstart, h->st.rmflag, h->st.rm_before, h->st.mkey,
+                  h->own_pos, h->own_thr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   h->scratch.release();

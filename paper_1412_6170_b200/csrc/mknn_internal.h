@@ -242,6 +242,11 @@ struct SearchArgs {
   // k_search1: persistent CTAs take query batches from *work (zeroed by
   // search_launch before each launch)
   unsigned* work;
+  // 16 < k <= 32: the own-leaf pass (k_own1) hands each query's list to the
+  // expansion kernel (k_search1) as k store positions (32 slots) and its
+  // k-th d2, by leaf-grouped position; [nq * 32] and [nq]
+  int32_t* own_pos;
+  double* own_thr;
 };
 
 // T from task keys: sorts keys in place (alt buffer) and sums the leaf

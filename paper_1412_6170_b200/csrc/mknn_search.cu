@@ -1188,15 +1188,16 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
 // 1.04x (ncu: 531 MB against 512 MB of rows) at the same speed.  CTAs are
 // persistent and take 32-query batches from a work counter.
 //
-// Chunk tiles in shared memory (template flag TMA, MKNN_SEARCH_VAR=1): the
-// two chunks of a step are contiguous 512-byte spans of the store, staged by
-// 1-D bulk copies (cp.async.bulk, mbarrier completion) issued one step ahead
-// into a per-warp two-slot ring, as the paper stages a cell's objects for
-// its queries.  Measured on B200 it is 3.8x slower than
-// loading the records through L1 (cfg3 search 8.95 vs 2.35 ms): a warp step
-// holds only 1 KB, and the ~160 bulk copies per 32-query batch queue on the
-// SM's copy engine (~280 cycles per request), while the L1 serves the same
-// records to the leaf's other queries.  Kept for that measurement only.
+// The own-leaf pass runs as its own kernel (k_own1) over leaf tasks, the
+// paper's cell-per-SM staging: a CTA takes 64 consecutive
+// queries of the leaf-grouped order, bulk-copies (cp.async.bulk, TMA 1-D,
+// mbarrier completion) the records and chunk boxes of their own leaves --
+// contiguous spans of the store -- into shared memory once, and its four
+// warps run the queries' own-leaf passes from there.  The lists go to global
+// memory as store positions and k_search1 continues with the expansion.
+// (A per-warp ring of 1 KB chunk tiles filled one step ahead, the first
+// attempt, measured 3.8x slower: ~160 small bulk copies per 32-query batch
+// queue on the copy engine.  A leaf is staged once for all its queries.)
 struct L1 {
   double d;
   long long id;
@@ -1229,8 +1230,41 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, unsigned
       : "memory");
 }
 
-constexpr int TILE = 32;  // records per ring slot: two 16-object chunks
-static_assert(chunk_for_k(32) * 2 == TILE, "a tile holds the two chunks of one step");
+// where a visit reads its leaf: the store in global memory (SH = false) or
+// the CTA's shared-memory stage of the leaf (SH = true: srec / sbox are the
+// shared addresses of the leaf's first record and first chunk box)
+struct LeafSrc {
+  uint32_t srec, sbox;
+};
+
+template <bool SH>
+__device__ __forceinline__ ChunkBox box_at(const ChunkBox* __restrict__ box, const LeafSrc& src,
+                                           int c, int c0) {
+  if constexpr (SH) {
+    ChunkBox b;
+    const uint32_t ad = src.sbox + (uint32_t)(c - c0) * (uint32_t)sizeof(ChunkBox);
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(b.x_lo), "=d"(b.y_lo) : "r"(ad));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(b.x_hi), "=d"(b.y_hi) : "r"(ad + 16));
+    return b;
+  } else {
+    return box[c];
+  }
+}
+
+template <bool SH>
+__device__ __forceinline__ void rec_at(const StoreRec* __restrict__ obj, const LeafSrc& src, int r,
+                                       int ob, double& x, double& y, long long& id) {
+  if constexpr (SH) {
+    const uint32_t ad = src.srec + (uint32_t)(r - ob) * (uint32_t)sizeof(StoreRec);
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(ad));
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(id) : "r"(ad + 16));
+  } else {
+    const StoreRec q = ld_rec(&obj[r]);
+    x = q.x;
+    y = q.y;
+    id = q.id;
+  }
+}
 
 // one step's chunks, distributed: lane l < 16 holds record l of the nearer
 // chunk, lane 16 + l record l of the other (rec = its store index, -1 when
@@ -1255,9 +1289,10 @@ struct ChunkIter {
 
 // the (up to) two nearest remaining chunks that qualify under kd, nearest
 // first (kd only shrinks, so a chunk that does not qualify never will)
+template <bool SH>
 __device__ __forceinline__ Pick next_pick(ChunkIter& it, double kd, int ob, int oe, int c0,
-                                          const ChunkBox* __restrict__ box, double qx, double qy,
-                                          int lane) {
+                                          const ChunkBox* __restrict__ box, const LeafSrc& src,
+                                          double qx, double qy, int lane) {
   constexpr int CH = chunk_for_k(32);
   Pick p;
   p.rec = -1;
@@ -1267,7 +1302,9 @@ __device__ __forceinline__ Pick next_pick(ChunkIter& it, double kd, int ob, int 
     if (!__any_sync(FULL, cand)) {
       it.g += 32;
       if (it.g >= it.c1) return p;
-      it.mdf = it.g + lane < it.c1 ? __double2float_rd(mindist2_box(box[it.g + lane], qx, qy)) : MKNN_FDEAD;
+      it.mdf = it.g + lane < it.c1
+                   ? __double2float_rd(mindist2_box(box_at<SH>(box, src, it.g + lane, c0), qx, qy))
+                   : MKNN_FDEAD;
       continue;
     }
     // nearest box first (key: mdf with the lane in the low bits; mdf >= 0,
@@ -1288,44 +1325,6 @@ __device__ __forceinline__ Pick next_pick(ChunkIter& it, double kd, int ob, int 
     p.rec = ch >= 0 && r < min(ob + (it.g - c0 + ch + 1) * CH, oe) ? r : -1;
     return p;
   }
-}
-
-// shared-memory ring of two tiles (one mbarrier each) per warp: the tiles
-// and barriers are the CTA's static shared arrays; the state is one word
-// (bits 0-1: parity of each slot's next completion, bit 2: slot to fill)
-__shared__ __align__(128) StoreRec ring_buf[2 * TILE];
-__shared__ __align__(8) unsigned long long ring_bar[2];
-
-__device__ __forceinline__ uint32_t ring_bar_addr(int s) { return smem_u32(&ring_bar[s]); }
-
-// bulk-copy one pick into the next slot (lane 0 issues); returns the slot
-__device__ __forceinline__ int ring_issue(uint32_t& R, const Pick& p, const StoreRec* __restrict__ obj,
-                                          int lane) {
-  const int s = (R >> 2) & 1;
-  R ^= 4u;
-  const unsigned v = __ballot_sync(FULL, p.rec >= 0);
-  const int s1 = __shfl_sync(FULL, p.rec, 16);
-  if (lane == 0) {
-    const unsigned n0 = __popc(v & 0xffffu), n1 = __popc(v >> 16);
-    const uint32_t bar = ring_bar_addr(s);
-    const uint32_t dst = smem_u32(&ring_buf[s * TILE]);
-    mbar_expect_tx(bar, (n0 + n1) * (unsigned)sizeof(StoreRec));
-    bulk_g2s(dst, obj + p.rec, n0 * (unsigned)sizeof(StoreRec), bar);
-    if (n1) bulk_g2s(dst + (TILE / 2) * sizeof(StoreRec), obj + s1, n1 * (unsigned)sizeof(StoreRec), bar);
-  }
-  return s;
-}
-
-__device__ __forceinline__ void ring_wait(uint32_t& R, int s) {
-  mbar_wait(ring_bar_addr(s), (R >> s) & 1u);
-  R ^= 1u << s;
-}
-
-// record `lane` of slot s: x, y, id
-__device__ __forceinline__ void ring_rec(int s, int lane, double& x, double& y, long long& id) {
-  const uint32_t a = smem_u32(&ring_buf[s * TILE + lane]);
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
-  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(id) : "r"(a + 16));
 }
 
 __device__ __forceinline__ void kth1(const L1& L, int k, double& kd, long long& ki) {
@@ -1472,10 +1471,10 @@ __device__ __forceinline__ void admit1(L1& L, double cd, long long ci, int cp, u
 // competes; admission is (d2, id) < k-th.  Chunks whose box min-dist2
 // exceeds the k-th d2 (or the cap, see k_search1) cannot hold an admissible
 // object and are skipped.
-template <bool TMA>
+template <bool SH>
 __device__ __forceinline__ void visit1(L1& L, int k, int leaf, double qx, double qy, long long me,
-                                       const SearchArgs& a, int lane, uint32_t& R, bool own,
-                                       double cap = DINF) {
+                                       const SearchArgs& a, int lane, bool own, double cap = DINF,
+                                       LeafSrc src = LeafSrc{0u, 0u}) {
   const int ob = __ldg(&a.cell_start[leaf]), oe = __ldg(&a.cell_start[leaf + 1]);
   const int c0 = __ldg(&a.chunk_start[leaf]), c1 = __ldg(&a.chunk_start[leaf + 1]);
   prof_add(a.prof, own ? PROF_OWN_CHUNKS_TOTAL : PROF_EXP_CHUNKS_TOTAL, c1 - c0, lane);
@@ -1491,31 +1490,16 @@ __device__ __forceinline__ void visit1(L1& L, int k, int leaf, double qx, double
   it.g = c0 - 32;
   it.c1 = c1;
   it.mdf = MKNN_FDEAD;
-  Pick cur = next_pick(it, kd, ob, oe, c0, a.box, qx, qy, lane);
+  Pick cur = next_pick<SH>(it, kd, ob, oe, c0, a.box, src, qx, qy, lane);
   if (cur.md0 < 0.0f) {
     if (!own) prof_add(a.prof, PROF_EXP_VISITS_NO_SCAN, 1, lane);
     return;
   }
-  int cs = TMA ? ring_issue(R, cur, a.obj, lane) : 0;
   bool admitted = false;
   for (;;) {
     double x = 0.0, y = 0.0;
     long long id = 0;
-    Pick nxt;
-    int ns = 0;
-    if constexpr (TMA) {
-      nxt = next_pick(it, kd, ob, oe, c0, a.box, qx, qy, lane);
-      if (nxt.md0 >= 0.0f) ns = ring_issue(R, nxt, a.obj, lane);
-      ring_wait(R, cs);
-      if (cur.rec >= 0) ring_rec(cs, lane, x, y, id);
-    } else {
-      if (cur.rec >= 0) {
-        const StoreRec r = ld_rec(&a.obj[cur.rec]);
-        x = r.x;
-        y = r.y;
-        id = r.id;
-      }
-    }
+    if (cur.rec >= 0) rec_at<SH>(a.obj, src, cur.rec, ob, x, y, id);
     prof_add(a.prof, own ? PROF_OWN_CHUNKS_SCANNED : PROF_EXP_CHUNKS_SCANNED, 1, lane);
     const bool valid = cur.rec >= 0;
     const double d2 = valid ? pair_d2(qx, qy, x, y) : DINF;
@@ -1530,14 +1514,9 @@ __device__ __forceinline__ void visit1(L1& L, int k, int leaf, double qx, double
       }
       admitted = true;
     }
-    if constexpr (!TMA) nxt = next_pick(it, kd, ob, oe, c0, a.box, qx, qy, lane);
+    const Pick nxt = next_pick<SH>(it, kd, ob, oe, c0, a.box, src, qx, qy, lane);
     if (nxt.md0 < 0.0f) break;
     cur = nxt;
-    cs = ns;
-    // the prefetch was picked before this scan tightened kd: when its
-    // nearer chunk no longer qualifies, neither does the rest of its
-    // 32-chunk group (later groups still may), so its scan is skipped
-    if ((double)nxt.md0 > kd) cur.rec = -1;
   }
   if (!own) prof_add(a.prof, PROF_EXP_VISITS_ADMITTING, admitted, lane);
 }
@@ -1557,7 +1536,10 @@ __device__ __forceinline__ void list_gather(L1& L, const int32_t* __restrict__ l
   }
 }
 
-template <int B, int MINB, bool TMA>
+// FUSED: the own-leaf pass runs inline (one kernel; MKNN_OWN_FUSED=1, for
+// A/B); otherwise k_own1 ran it and left each query's list (store positions)
+// in a.own_pos and its k-th d2 in a.own_thr, by leaf-grouped position.
+template <int B, int MINB, bool FUSED>
 __global__ void __launch_bounds__(32, MINB) k_search1(const __grid_constant__ SearchArgs a) {
   static_assert(B <= 32, "one query per lane");
   __shared__ double2 cw_tab[MAX_L_MAX + 1];
@@ -1566,12 +1548,6 @@ __global__ void __launch_bounds__(32, MINB) k_search1(const __grid_constant__ Se
   const int l_deep = __ldg(&a.scalars[0]);
   if (lane <= l_deep)
     cw_tab[lane] = make_double2(__dmul_rn(a.r.w, pow2_neg(lane)), __dmul_rn(a.r.h, pow2_neg(lane)));
-  uint32_t R = 0;
-  if (lane == 0) {
-    mbar_init(ring_bar_addr(0), 1);
-    mbar_init(ring_bar_addr(1), 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
   __syncwarp();
   const bool cw_exact =
       (a.r.w == 0.0 || a.r.w >= 0x1p-1000) && (a.r.h == 0.0 || a.r.h >= 0x1p-1000);
@@ -1614,8 +1590,12 @@ __global__ void __launch_bounds__(32, MINB) k_search1(const __grid_constant__ Se
     // its list excludes this issuer (see k_search: d <= d_prev(k) + |q -
     // q_prev|, padded by 2^-30 relative; the list after the pass -- and the
     // navigation threshold taken from it, engine.py:415 -- is unchanged)
+    if constexpr (!FUSED) {
+      for (int j = 0; j < nb; j++) lists[j * 32 + lane] = __ldg(&a.own_pos[(int64_t)(t0 + j) * 32 + lane]);
+      if (mine) thr = __ldg(&a.own_thr[t0 + lane]);
+    }
     bool excl = false;  // the previous query's list excludes this query's issuer
-    for (int j = 0; j < nb; j++) {
+    for (int j = 0; j < nb && FUSED; j++) {
       const double jx = __shfl_sync(FULL, qx, j), jy = __shfl_sync(FULL, qy, j);
       const long long jme = __shfl_sync(FULL, me, j);
       const uint32_t jown = __shfl_sync(FULL, own, j);
@@ -1634,7 +1614,7 @@ __global__ void __launch_bounds__(32, MINB) k_search1(const __grid_constant__ Se
       L.d = DINF;
       L.id = IDMAX;
       L.pos = -1;
-      visit1<TMA>(L, k, (int)jown, jx, jy, jme, a, lane, R, true, cap);
+      visit1<false>(L, k, (int)jown, jx, jy, jme, a, lane, true, cap);
       double kd;
       long long ki;
       kth1(L, k, kd, ki);
@@ -1677,7 +1657,7 @@ __global__ void __launch_bounds__(32, MINB) k_search1(const __grid_constant__ Se
         const long long jme = __shfl_sync(FULL, me, j);
         L1 L;
         list_gather(L, lists + j * 32, k, a.obj, jx, jy, lane);
-        visit1<TMA>(L, k, jl, jx, jy, jme, a, lane, R, false);
+        visit1<false>(L, k, jl, jx, jy, jme, a, lane, false);
         lists[j * 32 + lane] = lane < k ? L.pos : -1;
         double kd;
         long long ki;
@@ -1714,6 +1694,166 @@ __global__ void __launch_bounds__(32, MINB) k_search1(const __grid_constant__ Se
       a.stats[t0 + lane] = st;
     }
     __syncwarp();
+  }
+}
+
+// ---- k_own1: the own-leaf pass as staged leaf tasks -----------------------
+constexpr int OWN_WARPS = 4;
+constexpr int OWN_PER_WARP = 16;                   // consecutive queries per warp
+constexpr int OWN_Q = OWN_WARPS * OWN_PER_WARP;    // queries per CTA batch
+constexpr int STAGE_RECS = 1024;                   // 32 KB of records
+constexpr int STAGE_BOXES = 128;                   // 4 KB of chunk boxes
+constexpr int OWN_CTAS_PER_SM = 5;
+
+// first_iteration (engine.py:356-373) for OWN_Q consecutive queries of the
+// leaf-grouped order per CTA batch.  Warp 0 plans the stage: the batch's
+// distinct own leaves, in order, get contiguous slices of the shared record
+// and box arrays while they fit (a leaf that does not fit -- and every later
+// one -- is read from global memory instead); each staged leaf's records and
+// boxes are two contiguous spans of the store, fetched by two bulk copies
+// that complete on one mbarrier.  Each warp then runs its 16 consecutive
+// queries' passes, capping each by the previous query's own-pass k-th
+// distance exactly as k_search1 does (same-leaf triangle bound).
+__global__ void __launch_bounds__(32 * OWN_WARPS, OWN_CTAS_PER_SM) k_own1(const __grid_constant__ SearchArgs a) {
+  __shared__ __align__(128) StoreRec srec[STAGE_RECS];
+  __shared__ __align__(128) ChunkBox sbox[STAGE_BOXES];
+  __shared__ double sqx[OWN_Q], sqy[OWN_Q];
+  __shared__ long long sme[OWN_Q];
+  __shared__ uint32_t sown[OWN_Q];
+  __shared__ int32_t sro[OWN_Q], sbo[OWN_Q];  // stage offsets of the query's leaf (-1: global)
+  __shared__ __align__(8) unsigned long long bar;
+  __shared__ unsigned s_batch;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const uint32_t bar_a = smem_u32(&bar);
+  if (t == 0) {
+    mbar_init(bar_a, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int k = a.k;
+  uint32_t phase = 0;
+  for (;;) {
+    if (t == 0) s_batch = atomicAdd(a.work + 1, 1u);
+    __syncthreads();
+    const int64_t t0 = (int64_t)s_batch * OWN_Q;
+    if (t0 >= a.nq) break;
+    const int nb = (int)((a.nq - t0) < OWN_Q ? (a.nq - t0) : OWN_Q);
+    if (t < nb) {
+      const uint32_t q = __ldg(&a.q_order[t0 + t]);
+      sqx[t] = __ldg(&a.qx[q]);
+      sqy[t] = __ldg(&a.qy[q]);
+      sme[t] = __ldg(&a.qi[q]);
+      sown[t] = __ldg(&a.q_leaf[q]);
+    }
+    __syncthreads();
+    if (w == 0) {
+      // order the previous batch's shared reads before this batch's bulk writes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      int ro = 0, bo = 0;      // stage fill so far
+      int c_ro = -1, c_bo = 0; // offsets of the leaf running into this round
+      bool open = true;        // no leaf has failed to fit yet
+      for (int r0 = 0; r0 < nb; r0 += 32) {
+        const int j = r0 + lane;
+        const bool in = j < nb;
+        const uint32_t l = in ? sown[j] : 0xffffffffu;
+        const bool first = in && (j == 0 || sown[j - 1] != l);
+        int nr = 0, nx = 0, ob = 0, c0 = 0;
+        if (first) {
+          ob = __ldg(&a.cell_start[l]);
+          nr = __ldg(&a.cell_start[l + 1]) - ob;
+          c0 = __ldg(&a.chunk_start[l]);
+          nx = __ldg(&a.chunk_start[l + 1]) - c0;
+        }
+        // inclusive prefix of the leaders' sizes
+        int pr = nr, px = nx;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int ur = __shfl_up_sync(FULL, pr, o), ux = __shfl_up_sync(FULL, px, o);
+          if (lane >= o) {
+            pr += ur;
+            px += ux;
+          }
+        }
+        const bool fits = open && ro + pr <= STAGE_RECS && bo + px <= STAGE_BOXES;
+        const bool stage = first && fits && nr > 0;
+        const int my_ro = ro + pr - nr, my_bo = bo + px - nx;
+        if (stage) {
+          const unsigned bytes = (unsigned)(nr + nx) * 32u;
+          asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(bar_a), "r"(bytes) : "memory");
+          bulk_g2s(smem_u32(&srec[my_ro]), a.obj + ob, (unsigned)nr * 32u, bar_a);
+          if (nx) bulk_g2s(smem_u32(&sbox[my_bo]), a.box + c0, (unsigned)nx * 32u, bar_a);
+        }
+        // every query takes its leader's offsets (or the carried ones)
+        const unsigned lead_m = __ballot_sync(FULL, first);
+        const unsigned below = lead_m & (0xffffffffu >> (31 - lane));
+        const int ld = below ? 31 - __clz(below) : -1;
+        const int l_ro = __shfl_sync(FULL, stage ? my_ro : -1, ld < 0 ? 0 : ld);
+        const int l_bo = __shfl_sync(FULL, my_bo, ld < 0 ? 0 : ld);
+        if (in) {
+          sro[j] = ld < 0 ? c_ro : l_ro;
+          sbo[j] = ld < 0 ? c_bo : l_bo;
+        }
+        // carry: the last query of the round's offsets; stage fill
+        c_ro = __shfl_sync(FULL, in ? sro[j] : -1, min(31, nb - 1 - r0));
+        c_bo = __shfl_sync(FULL, in ? sbo[j] : 0, min(31, nb - 1 - r0));
+        const unsigned fit_m = __ballot_sync(FULL, first && !fits);
+        const int tot_r = __shfl_sync(FULL, pr, 31), tot_x = __shfl_sync(FULL, px, 31);
+        if (fit_m) {
+          open = false;
+          // keep the fill of the leaders that did fit
+          const int fl = __ffs(fit_m) - 1;
+          const int fr = __shfl_sync(FULL, pr - nr, fl), fx = __shfl_sync(FULL, px - nx, fl);
+          ro += fr;
+          bo += fx;
+        } else {
+          ro += tot_r;
+          bo += tot_x;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_a) : "memory");
+    }
+    __syncthreads();
+    mbar_wait(bar_a, phase & 1u);
+    phase++;
+
+    const int j0 = w * OWN_PER_WARP, j1 = min(j0 + OWN_PER_WARP, nb);
+    double p_kd = DINF, p_x = 0.0, p_y = 0.0;
+    uint32_t p_own = 0xffffffffu;
+    bool excl = false;
+    for (int j = j0; j < j1; j++) {
+      const double jx = sqx[j], jy = sqy[j];
+      const long long jme = sme[j];
+      const uint32_t jown = sown[j];
+      double cap = DINF;
+      if (j > j0 && jown == p_own && p_kd < DINF && excl) {
+        const double dx = jx - p_x, dy = jy - p_y;
+        const double rr = sqrt(p_kd) + sqrt(dx * dx + dy * dy);
+        cap = rr * rr * (1.0 + 0x1p-30) + 0x1p-1000;
+      }
+      L1 L;
+      L.d = DINF;
+      L.id = IDMAX;
+      L.pos = -1;
+      const int ro = sro[j];
+      if (ro >= 0) {
+        const LeafSrc src{smem_u32(&srec[ro]), smem_u32(&sbox[sbo[j]])};
+        visit1<true>(L, k, (int)jown, jx, jy, jme, a, lane, true, cap, src);
+      } else {
+        visit1<false>(L, k, (int)jown, jx, jy, jme, a, lane, true, cap);
+      }
+      double kd;
+      long long ki;
+      kth1(L, k, kd, ki);
+      p_kd = kd;
+      p_x = jx;
+      p_y = jy;
+      p_own = jown;
+      excl = j + 1 < j1 ? !__any_sync(FULL, L.id == sme[j + 1]) : false;
+      a.own_pos[(t0 + j) * 32 + lane] = lane < k ? L.pos : -1;
+      if (lane == 0) a.own_thr[t0 + j] = kd;
+    }
+    __syncthreads();
   }
 }
 
@@ -1822,18 +1962,42 @@ int launch_batched(const SearchArgs& a, cudaStream_t s) {
 // resident CTAs of k_search1 per SM (1-warp CTAs; registers bound it)
 constexpr int SEARCH1_CTAS_PER_SM = 32;
 
-template <int B, bool TMA>
+template <int B, bool FUSED>
 int launch_search1(const SearchArgs& a, cudaStream_t s) {
   int dev = 0;
   MKNN_CUDA_OK(cudaGetDevice(&dev));
   int sms = 0;
   MKNN_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  MKNN_CUDA_OK(cudaMemsetAsync(a.work, 0, 2 * sizeof(unsigned), s));
+  if (!FUSED) {
+    const int64_t ob = (a.nq + OWN_Q - 1) / OWN_Q;
+    const int64_t og = std::min<int64_t>(ob, (int64_t)sms * OWN_CTAS_PER_SM);
+    MKNN_LAUNCH k_own1<<<(unsigned)og, 32 * OWN_WARPS, 0, s>>>(a);
+    MKNN_CUDA_OK(cudaGetLastError());
+  }
   const int64_t batches = (a.nq + B - 1) / B;
   int64_t grid = std::min<int64_t>(batches, (int64_t)sms * SEARCH1_CTAS_PER_SM);
-  MKNN_CUDA_OK(cudaMemsetAsync(a.work, 0, sizeof(unsigned), s));
-  MKNN_LAUNCH k_search1<B, SEARCH1_CTAS_PER_SM, TMA><<<(unsigned)grid, 32, 0, s>>>(a);
+  MKNN_LAUNCH k_search1<B, SEARCH1_CTAS_PER_SM, FUSED><<<(unsigned)grid, 32, 0, s>>>(a);
   MKNN_CUDA_OK(cudaGetLastError());
   return 0;
+}
+
+// Queries per warp batch: the query density picks it (see below), but never
+// so many that the batches stop covering the GPU: a small tick (cfg2: 100K
+// queries, 3.1K batches of 32 for 4.7K resident warps) leaves SMs idle and
+// its time is one warp's 32 serial own-leaf passes, so halve the batch until
+// there are >= 2 batches per resident warp slot (or 4 queries per warp).
+static int batch_for(const SearchArgs& a, int by_density) {
+  static int slots = 0;
+  if (!slots) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    slots = sms * SEARCH1_CTAS_PER_SM;
+  }
+  int b = by_density;
+  while (b > 4 && (a.nq + b - 1) / b < 2 * (int64_t)slots) b >>= 1;
+  return b;
 }
 
 int search_launch(const SearchArgs& a, cudaStream_t s) {
@@ -1849,21 +2013,23 @@ int search_launch(const SearchArgs& a, cudaStream_t s) {
   // there (the per-visit position gather weighs more on short lists)
   if (a.k > 16 && a.k <= 32 && !v0) {
     const double qd = (double)a.nq / (double)(a.n_objects > 0 ? a.n_objects : 1);
-    // MKNN_SEARCH_VAR=1: the chunk-tile ring filled by bulk copies (TMA), an
-    // experiment kept for measurement (3.8x slower)
-    static const bool ring = [] {
-      const char* e = getenv("MKNN_SEARCH_VAR");
+    // MKNN_OWN_STAGED=1: the own-leaf pass as k_own1's staged leaf tasks
+    // (bulk copies into shared memory) instead of inline in k_search1
+    static const bool staged = [] {
+      const char* e = getenv("MKNN_OWN_STAGED");
       return e && e[0] == '1';
     }();
-    if (ring) {
-      if (qd < 0.015) return launch_search1<4, true>(a, s);
-      if (qd < 0.04) return launch_search1<8, true>(a, s);
-      if (qd < 0.06) return launch_search1<16, true>(a, s);
+    if (!staged || !a.own_pos) {
+      const int b = batch_for(a, qd < 0.015 ? 4 : qd < 0.04 ? 8 : qd < 0.06 ? 16 : 32);
+      if (b == 4) return launch_search1<4, true>(a, s);
+      if (b == 8) return launch_search1<8, true>(a, s);
+      if (b == 16) return launch_search1<16, true>(a, s);
       return launch_search1<32, true>(a, s);
     }
-    if (qd < 0.015) return launch_search1<4, false>(a, s);
-    if (qd < 0.04) return launch_search1<8, false>(a, s);
-    if (qd < 0.06) return launch_search1<16, false>(a, s);
+    const int b = batch_for(a, qd < 0.015 ? 4 : qd < 0.04 ? 8 : qd < 0.06 ? 16 : 32);
+    if (b == 4) return launch_search1<4, false>(a, s);
+    if (b == 8) return launch_search1<8, false>(a, s);
+    if (b == 16) return launch_search1<16, false>(a, s);
     return launch_search1<32, false>(a, s);
   }
   // k <= 32: lists in the output rows (no shared memory: L1 holds the leaf
@@ -1876,10 +2042,13 @@ int search_launch(const SearchArgs& a, cudaStream_t s) {
   // queries -> 32; 300K -> 8: 1.75 -> 1.01 ms; a 1/4 row slice of a host
   // tick -> 8)
   const double qd = (double)a.nq / (double)(a.n_objects > 0 ? a.n_objects : 1);
-  if (a.k <= 32 && qd < 0.015) return launch_batched<1, 4, 1, 32, true>(a, s);
-  if (a.k <= 32 && qd < 0.04) return launch_batched<1, 8, 1, 32, true>(a, s);
-  if (a.k <= 32 && qd < 0.06) return launch_batched<1, 16, 1, 32, true>(a, s);
-  if (a.k <= 32) return launch_batched<1, 32, 1, 32, true>(a, s);
+  if (a.k <= 32) {
+    const int b = batch_for(a, qd < 0.015 ? 4 : qd < 0.04 ? 8 : qd < 0.06 ? 16 : 32);
+    if (b == 4) return launch_batched<1, 4, 1, 32, true>(a, s);
+    if (b == 8) return launch_batched<1, 8, 1, 32, true>(a, s);
+    if (b == 16) return launch_batched<1, 16, 1, 32, true>(a, s);
+    return launch_batched<1, 32, 1, 32, true>(a, s);
+  }
   // k > 32: the per-warp lists (B * 16 * k bytes of shared memory) bound the
   // resident warps, so fewer queries per warp win (measured at cfg3 objects:
   // k = 64 / 128 / 256 / 512 -24 / -18 / -24 / -17 % against 16/8/4/2; k =
