@@ -340,7 +340,8 @@ int alloc_store(mknn_engine* h, int64_t n) {
   if (n > h->st.cap) {
     int64_t nc = std::max<int64_t>(n, h->st.cap * 3 / 2);
     void** old[] = {(void**)&h->st.obj, (void**)&h->st.rec, (void**)&h->st.key,
-                    (void**)&h->st.rmflag, (void**)&h->st.rm_before, (void**)&h->st.mkey};
+                    (void**)&h->st.rmflag, (void**)&h->st.rm_before, (void**)&h->st.mkey,
+                    (void**)&h->st.slot_pos, (void**)&h->st.deferred};
     for (auto p : old) {
       cudaFree(*p);
       *p = nullptr;
@@ -353,6 +354,9 @@ int alloc_store(mknn_engine* h, int64_t n) {
     MKNN_CUDA_OK(cudaMalloc(&h->st.rmflag, sizeof(int32_t) * (nc + 1)));
     MKNN_CUDA_OK(cudaMalloc(&h->st.rm_before, sizeof(int32_t) * (nc + 2)));
     MKNN_CUDA_OK(cudaMalloc(&h->st.mkey, sizeof(uint32_t) * nc));
+    MKNN_CUDA_OK(cudaMalloc(&h->st.slot_pos, sizeof(int32_t) * nc));
+    MKNN_CUDA_OK(cudaMalloc(&h->st.deferred, sizeof(int32_t) * nc));
+    if (!h->st.n_deferred) MKNN_CUDA_OK(cudaMalloc(&h->st.n_deferred, sizeof(int32_t)));
     h->st.cap = nc;
   }
   return 0;
@@ -990,7 +994,7 @@ void mknn_destroy(mknn_engine* h) {
                   h->tk, h->tk_alt, h->tk_cnt, h->tv, h->tv_alt, h->prof, h->mark, h->moved,
                   h->d_nmoved, h->clamped_total, h->work, h->st.kstart_alt, h->st.fill,
                   h->st.qcnt, h->st.qkstart, h->st.rmflag, h->st.rm_before, h->st.mkey,
-                  h->own_pos, h->own_thr};
+                  h->own_pos, h->own_thr, h->st.slot_pos, h->st.deferred, h->st.n_deferred};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   h->scratch.release();

@@ -332,7 +332,19 @@ __device__ __forceinline__ bool outside(double x, double y, const Region& r) {
 
 // moved slot j: remove its old record (if it had one: found in its old key
 // group, a handful of records, by the slot the record carries), key its new
-// position; slot_key[slot] is every slot's key at the last (re)index
+// position; slot_key[slot] is every slot's key at the last (re)index.  A
+// group longer than SCAN_MAX (dense clusters, coincident points) is not
+// scanned: j is deferred to k_moved_deferred, which looks the record up in
+// a slot -> position map that k_slot_map builds only when something was
+// deferred (both return at once otherwise).
+constexpr int SCAN_MAX = 64;
+
+__device__ __forceinline__ void remove_old(int32_t p, const StoreRec* __restrict__ obj, const Region& r,
+                                           int32_t* __restrict__ rmflag, unsigned long long* clamped) {
+  rmflag[p] = 1;
+  if (outside(obj[p].x, obj[p].y, r)) atomicAdd(clamped, ~0ull);  // -1
+}
+
 __global__ void k_moved_keys(const int32_t* __restrict__ moved, int64_t m, int64_t n_old_slots,
                              uint32_t* __restrict__ slot_key, const int32_t* __restrict__ kold,
                              const StoreRec* __restrict__ obj, const double* __restrict__ sx,
@@ -340,18 +352,23 @@ __global__ void k_moved_keys(const int32_t* __restrict__ moved, int64_t m, int64
                              const int32_t* __restrict__ scalars,
                              const unsigned long long* __restrict__ info,
                              int32_t* __restrict__ rmflag, int32_t* __restrict__ cnt,
-                             uint32_t* __restrict__ mkey, unsigned long long* clamped) {
+                             uint32_t* __restrict__ mkey, unsigned long long* clamped,
+                             int32_t* __restrict__ deferred, int32_t* __restrict__ n_deferred) {
   const int l_deep = scalars[0];
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m;
        j += (int64_t)gridDim.x * blockDim.x) {
     const int32_t sl = moved[j];
     if (sl < n_old_slots) {
       const uint32_t ok = slot_key[sl];
-      for (int32_t p = kold[ok], e = kold[ok + 1]; p < e; p++) {
-        if ((int32_t)obj[p].pad == sl) {
-          rmflag[p] = 1;
-          if (outside(obj[p].x, obj[p].y, r)) atomicAdd(clamped, ~0ull);  // -1
-          break;
+      const int32_t b = kold[ok], e = kold[ok + 1];
+      if (e - b > SCAN_MAX) {
+        deferred[atomicAdd(n_deferred, 1)] = sl;
+      } else {
+        for (int32_t p = b; p < e; p++) {
+          if ((int32_t)obj[p].pad == sl) {
+            remove_old(p, obj, r, rmflag, clamped);
+            break;
+          }
         }
       }
       atomicSub(&cnt[ok], 1);
@@ -364,6 +381,25 @@ __global__ void k_moved_keys(const int32_t* __restrict__ moved, int64_t m, int64
     atomicAdd(&cnt[key], 1);
     if (outside(x, y, r)) atomicAdd(clamped, 1ull);
   }
+}
+
+__global__ void k_slot_map(const StoreRec* __restrict__ obj, int64_t n_old,
+                           const int32_t* __restrict__ n_deferred, int32_t* __restrict__ slot_pos) {
+  if (*n_deferred == 0) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_old;
+       i += (int64_t)gridDim.x * blockDim.x)
+    slot_pos[obj[i].pad] = (int32_t)i;
+}
+
+__global__ void k_moved_deferred(const int32_t* __restrict__ deferred,
+                                 const int32_t* __restrict__ n_deferred,
+                                 const int32_t* __restrict__ slot_pos,
+                                 const StoreRec* __restrict__ obj, Region r,
+                                 int32_t* __restrict__ rmflag, unsigned long long* clamped) {
+  const int64_t nd = *n_deferred;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nd;
+       j += (int64_t)gridDim.x * blockDim.x)
+    remove_old(slot_pos[deferred[j]], obj, r, rmflag, clamped);
 }
 
 __global__ void k_move_survivors(const StoreRec* __restrict__ obj, int64_t n_old,
@@ -748,10 +784,16 @@ int store_update_incremental(DevStore& st, const DevIndex& ix, const Region& r,
   MKNN_LAUNCH k_key_counts<<<grid_stride_blocks(n_sub), TPB, 0, s>>>(st.kstart, n_sub, st.cnt);
   st.dirty = true;  // cnt no longer all zero
   MKNN_CUDA_OK(cudaMemsetAsync(st.rmflag, 0, sizeof(int32_t) * (n_old + 1), s));
-  if (m > 0)
+  if (m > 0) {
+    MKNN_CUDA_OK(cudaMemsetAsync(st.n_deferred, 0, sizeof(int32_t), s));
     MKNN_LAUNCH k_moved_keys<<<grid_stride_blocks(m), TPB, 0, s>>>(
         moved, m, n_old, st.key, st.kstart, st.obj, sx, sy, r, ix.scalars, ix.cell_info, st.rmflag,
-        st.cnt, st.mkey, dev_clamped_total);
+        st.cnt, st.mkey, dev_clamped_total, st.deferred, st.n_deferred);
+    MKNN_LAUNCH k_slot_map<<<grid_stride_blocks(n_old), TPB, 0, s>>>(st.obj, n_old, st.n_deferred,
+                                                                    st.slot_pos);
+    MKNN_LAUNCH k_moved_deferred<<<grid_stride_blocks(m), TPB, 0, s>>>(
+        st.deferred, st.n_deferred, st.slot_pos, st.obj, r, st.rmflag, dev_clamped_total);
+  }
   MKNN_CUDA_OK(cudaGetLastError());
   int rc = exclusive_scan_i32(st.cnt, st.kstart_alt, n_sub, scratch, s);
   if (rc) return rc;

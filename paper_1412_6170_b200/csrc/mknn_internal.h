@@ -139,6 +139,11 @@ struct DevStore {
   int32_t* rmflag = nullptr;      // cap + 1: incremental update scratch
   int32_t* rm_before = nullptr;   // cap + 1
   uint32_t* mkey = nullptr;       // cap: new keys of the moved slots
+  // moved slots whose old key group is large (dense or coincident points):
+  // found through a slot -> store position map built only when needed
+  int32_t* slot_pos = nullptr;    // cap
+  int32_t* deferred = nullptr;    // cap: indices into the moved list
+  int32_t* n_deferred = nullptr;  // device counter
   int64_t n_store = 0;            // records in obj
   bool valid = false;             // obj/kstart mirror the engine's snapshot (delta path)
   int chunk = 32;                 // objects per chunk (chunk_for_k)

@@ -146,6 +146,30 @@ _CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the legacy NULL stream as a handle
 _POOL = None
 
 
+def _host_out(nq: int, k: int):
+    """Fresh result arrays for a host tick, owned by the caller (engine.py's
+    TickResult arrays are new per tick).  They are page-locked so the
+    library's per-slice device->host copies run asynchronously and overlap
+    the next slice's search: a copy into pageable memory blocks the host
+    until it completes.  torch's pinned caching allocator recycles a block
+    once every array viewing it is gone, so steady-state ticks allocate no
+    new page-locked memory; without CUDA (never on the product path, which
+    needs a device) plain arrays are returned."""
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            def pinned(n, dt):
+                return torch.empty(max(n, 1), dtype=dt, pin_memory=True).numpy()[:n]
+
+            return (pinned(nq, torch.int64), pinned(nq, torch.int32), pinned(nq * k, torch.int64),
+                    pinned(nq * k, torch.float64))
+    except ImportError:  # pragma: no cover - torch is part of the runtime
+        pass
+    return (np.empty(nq, np.int64), np.empty(nq, np.int32), np.empty(nq * k, np.int64),
+            np.empty(nq * k, np.float64))
+
+
 def _parallel_fill(fn, n: int, min_chunk: int = 1 << 17) -> None:
     """fn(lo, hi) over [0, n) in chunks on a small thread pool (numpy
     releases the GIL): the 8 MB offsets array of a 1M-query tick costs ~1 ms
@@ -355,13 +379,7 @@ class Engine:
         n, nq = len(ids), len(q_issuer)
         if len(x) != n or len(y) != n or len(qx) != nq or len(qy) != nq:
             raise ValueError("coordinate arrays must match the id arrays in length")
-        if out is None:
-            qids = np.empty(nq, np.int64)
-            lens = np.empty(nq, np.int32)
-            nids = np.empty(nq * k, np.int64)
-            dist = np.empty(nq * k, np.float64)
-        else:
-            qids, lens, nids, dist = out[:4]
+        qids, lens, nids, dist = out[:4] if out is not None else _host_out(nq, k)
         m = N.Metrics()
         N.check(N.lib().mknn_tick(h, n, _ptr(ids), _ptr(x), _ptr(y), nq, _ptr(q_issuer), _ptr(qx),
                                   _ptr(qy), _ptr(qids), _ptr(lens), _ptr(nids), _ptr(dist),
@@ -442,13 +460,7 @@ class Engine:
         qx = np.ascontiguousarray(qx, dtype=np.float64)
         qy = np.ascontiguousarray(qy, dtype=np.float64)
         nq = len(q_issuer)
-        if out is None:
-            qids = np.empty(nq, np.int64)
-            lens = np.empty(nq, np.int32)
-            nids = np.empty(nq * k, np.int64)
-            dist = np.empty(nq * k, np.float64)
-        else:
-            qids, lens, nids, dist = out[:4]
+        qids, lens, nids, dist = out[:4] if out is not None else _host_out(nq, k)
         m = N.Metrics()
         N.check(N.lib().mknn_query(h, nq, _ptr(q_issuer), _ptr(qx), _ptr(qy), _ptr(qids),
                                    _ptr(lens), _ptr(nids), _ptr(dist), ctypes.byref(m)), h,

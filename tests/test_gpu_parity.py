@@ -444,17 +444,27 @@ def test_cfg4_full_size_vs_engine_port():
     assert m.pruned_leaves == want.metrics["pruned_leaves"]
 
 
-@pytest.mark.parametrize("dist", ["uniform", "gaussian"])
+@pytest.mark.parametrize("dist", ["uniform", "gaussian", "coincident"])
 def test_incremental_store_matches_full_rebuild(dist):
     """Delta ticks re-index incrementally (only the moved slots change key):
     over many ticks -- repeated updates of an id between queries, updates
     in several batches, new ids appended, moves out of / back into the
     region, a query with no update -- every result and metric (incl.
     clamped_objects) equals a full-snapshot tick on the carried-forward
-    snapshot."""
+    snapshot.  "coincident": 40 % of the objects sit on 20 shared points and
+    updates move objects onto / off them, so old key groups far longer than
+    the scanned limit take the slot -> position map path (k_moved_deferred)."""
     rng = np.random.default_rng(7)
     n = 40_000
-    snap = synth.place(n, dist, seed=12, hotspots=5, sigma=700.0)
+    spots = None
+    if dist == "coincident":
+        snap = synth.place(n, "uniform", seed=12)
+        spots = rng.uniform(0, 22500, (20, 2))
+        on = rng.random(n) < 0.4
+        pick = rng.integers(0, 20, n)
+        snap.x[on], snap.y[on] = spots[pick[on], 0], spots[pick[on], 1]
+    else:
+        snap = synth.place(n, dist, seed=12, hotspots=5, sigma=700.0)
     ids = list(snap.ids)
     xs, ys = list(snap.x), list(snap.y)
     pos = {int(i): j for j, i in enumerate(snap.ids)}
@@ -467,6 +477,10 @@ def test_incremental_store_matches_full_rebuild(dist):
                 uid = rng.choice(np.asarray(ids), u, replace=True)  # repeats inside a batch
                 ux = rng.uniform(-800, 23300, u)  # some outside the region [0, 22500]
                 uy = rng.uniform(-800, 23300, u)
+                if spots is not None:  # half of the moves land on a shared point
+                    on = rng.random(u) < 0.5
+                    pick = rng.integers(0, 20, u)
+                    ux[on], uy[on] = spots[pick[on], 0], spots[pick[on], 1]
                 if rng.random() < 0.5:  # brand-new ids
                     new = np.arange(10 ** 9 + len(ids), 10 ** 9 + len(ids) + 7)
                     uid = np.concatenate([uid, new])

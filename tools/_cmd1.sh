@@ -1,2 +1,3 @@
-WLS="gaussian 1e7 1e6 32|uniform 1e7 1e6 32" VARS="MKNN_PREFILL=0 MKNN_PREFILL=1 MKNN_PREFILL=2" bash tools/gpu_ab2.sh pre2
-WLS="gaussian 1e7 1e6 16|gaussian 1e7 1e6 8|uniform 1e7 1e6 16" VARS="MKNN_K16_SEARCH1=0 MKNN_K16_SEARCH1=1" bash tools/gpu_ab2.sh k16
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -x --durations=10 > gpurun_out/pytest_r2b.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_r2b.log
+tail -15 gpurun_out/pytest_r2b.log
