@@ -130,6 +130,11 @@ int mknn_query_device(mknn_engine* h, int64_t nq, const int64_t* d_q_issuer, con
 
 /* Toggle instrumentation (mknn_config.instrument bits) between ticks. */
 int mknn_set_instrument(mknn_engine* h, int32_t flags);
+/* Steady-state device ticks (same shape, buffers and flags as the previous
+ * one) replay a CUDA graph of the whole tick; counts of graph captures and
+ * replays on this handle so far (no reference counterpart: the reference
+ * has no device). */
+int mknn_graph_stats(const mknn_engine* h, int64_t* captures, int64_t* replays);
 
 /* Multi-GPU: replace the last tick's entry of the rebuild history
  * (quadindex.py:231-246 input, engine.py:692) with the job-wide

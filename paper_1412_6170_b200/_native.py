@@ -68,6 +68,7 @@ SIGNATURES = {
     "mknn_query_device": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                          _vp, ctypes.POINTER(Metrics)]),
     "mknn_set_instrument": (ctypes.c_int, [_vp, ctypes.c_int32]),
+    "mknn_graph_stats": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
     "mknn_set_last_evals": (ctypes.c_int, [_vp, ctypes.c_int64]),
     "mknn_active_counts": (ctypes.c_int64, [_vp, ctypes.c_int, _i64p, ctypes.c_int64]),
     "mknn_index_info": (ctypes.c_int, [_vp, _i32p, _i64p, _i64p, _i64p]),

@@ -19,6 +19,7 @@ const char* last_error_text();
 // number of our own launches inside its timed region)
 void note_launch();
 long long launch_count();
+void note_launches(long long n);  // a graph replay: its captured kernels
 #define MKNN_LAUNCH ::mknn::note_launch(),
 
 // error codes (C-ABI: 0 ok, < 0 error)

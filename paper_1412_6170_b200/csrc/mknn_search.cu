@@ -526,8 +526,8 @@ __device__ __forceinline__ bool akey32_ties(const uint32_t (&kk)[KPL], int bits,
 
 // exact (d2, id) fallback of merge_buffer (equal truncated keys)
 template <int KPL>
-__device__ __noinline__ void merge_buffer_exact(List<KPL>& L, const double* bufd,
-                                                const long long* bufi, int nbuf, int lane) {
+__device__ __noinline__ List<KPL> merge_buffer_exact(List<KPL> L, const double* bufd,
+                                                     const long long* bufi, int nbuf, int lane) {
   double cd[KPL];
   long long ci[KPL];
 #pragma unroll
@@ -539,6 +539,7 @@ __device__ __noinline__ void merge_buffer_exact(List<KPL>& L, const double* bufd
   bitonic_sort<KPL>(cd, ci, lane);
   bitonic_merge_into<KPL>(L, cd, ci, lane);
   __syncwarp();
+  return L;
 }
 
 // Odd-even transposition on the exact (d2, id) order until sorted.  The
@@ -638,7 +639,7 @@ __device__ __forceinline__ void merge_buffer32(List<KPL>& L, const double* bufd,
   for (int j = N >> 1; j > 0; j >>= 1) step_key<KPL>(m, lane, N, j);
   __syncwarp();
   if (cut_tie) {
-    merge_buffer_exact<KPL>(L, bufd, bufi, nbuf, lane);
+    L = merge_buffer_exact<KPL>(L, bufd, bufi, nbuf, lane);
     return;
   }
   // k <= 64 (16 key bits): truncated ties are rare, the exact networks
@@ -646,7 +647,7 @@ __device__ __forceinline__ void merge_buffer32(List<KPL>& L, const double* bufd,
   // merge, repaired in place
   const bool ties = akey32_ties<KPL>(m, SB, lane);
   if (KPL < 4 && ties) {
-    merge_buffer_exact<KPL>(L, bufd, bufi, nbuf, lane);
+    L = merge_buffer_exact<KPL>(L, bufd, bufi, nbuf, lane);
     return;
   }
 #pragma unroll
@@ -663,8 +664,8 @@ __device__ __forceinline__ void merge_buffer32(List<KPL>& L, const double* bufd,
 // L <- the N smallest of L u buffer[0, nbuf); L ascending.  rowd/rowi: the
 // list's shared-memory home (overwritten), bufd/bufi: the buffer.
 template <int KPL>
-__device__ __noinline__ void merge_buffer(List<KPL>& L, const double* bufd, const long long* bufi,
-                                          int nbuf, double* rowd, long long* rowi, int lane) {
+__device__ __noinline__ List<KPL> merge_buffer(List<KPL> L, const double* bufd, const long long* bufi,
+                                               int nbuf, double* rowd, long long* rowi, int lane) {
   constexpr int N = 32 * KPL;
   constexpr int SB = KPL <= 2 ? 7 : (KPL <= 4 ? 8 : (KPL <= 8 ? 9 : 10));  // bits for 2N sources
   unsigned long long kb[KPL], m[KPL];
@@ -711,7 +712,7 @@ __device__ __noinline__ void merge_buffer(List<KPL>& L, const double* bufd, cons
     bitonic_sort<KPL>(cd, ci, lane);
     bitonic_merge_into<KPL>(L, cd, ci, lane);
     __syncwarp();
-    return;
+    return L;
   }
 #pragma unroll
   for (int s = 0; s < KPL; s++) {
@@ -721,6 +722,7 @@ __device__ __noinline__ void merge_buffer(List<KPL>& L, const double* bufd, cons
     L.id[s] = from_list ? rowi[src] : (pad ? IDMAX : bufi[src - N]);
   }
   __syncwarp();
+  return L;
 }
 
 // KPL <= 4 (k <= 128): 32-bit keys (>= 15 mantissa bits); wider lists merge
@@ -733,7 +735,7 @@ __device__ __forceinline__ void merge_buffer_k(List<KPL>& L, const double* bufd,
   if constexpr (KPL <= 4)
     merge_buffer32<KPL>(L, bufd, bufi, nbuf, rowd, rowi, lane);
   else
-    merge_buffer<KPL>(L, bufd, bufi, nbuf, rowd, rowi, lane);
+    L = merge_buffer<KPL>(L, bufd, bufi, nbuf, rowd, rowi, lane);
 }
 
 template <int KPL>

@@ -256,6 +256,13 @@ class Engine:
         if self._h is not None:
             N.check(N.lib().mknn_set_instrument(self._h, int(self._instrument)), self._h)
 
+    @property
+    def graph_stats(self):
+        """(captures, replays) of the steady-state tick graph on this engine."""
+        c, r = ctypes.c_int64(), ctypes.c_int64()
+        N.check(N.lib().mknn_graph_stats(self._handle(), ctypes.byref(c), ctypes.byref(r)), self._h)
+        return c.value, r.value
+
     def set_stream(self, stream) -> None:
         """Run on a torch.cuda.Stream (or a raw cudaStream_t int; 0/None =
         the engine's own stream).  torch's default stream is the legacy NULL

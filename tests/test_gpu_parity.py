@@ -193,6 +193,70 @@ def test_device_tensors_path():
     assert out["distances"][:nres].cpu().numpy().tobytes() == host.distances.tobytes()
 
 
+@pytest.mark.parametrize("k", [16, 32])
+def test_graph_replay_equals_direct(k):
+    """Steady-state device ticks replay a captured CUDA graph: every replay
+    -- on new contents of the same input buffers, and on the delta path
+    (update + query_device over the engine's snapshot) -- equals the direct
+    host path (never graphed) on the same data, results and metrics."""
+    rng = np.random.default_rng(11)
+    snap = synth.place(60_000, "gaussian", seed=4, hotspots=6)
+    qi, qx, qy = synth.queries(snap, 6000, seed=4)
+    dev = torch.device("cuda:0")
+    T = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)  # noqa: E731
+    d = [T(a) for a in (snap.ids, snap.x, snap.y, qi, qx, qy)]
+    keys = ("distance_evals", "pruned_leaves", "active_left", "active_right", "rebuild_flag")
+    with Engine(EngineConfig(k=k, region=synth.REGION)) as g, \
+            Engine(EngineConfig(k=k, region=synth.REGION)) as ref:
+        out = None
+        x, y = snap.x.copy(), snap.y.copy()
+        for t in range(6):
+            if t >= 3:  # new positions in the same device buffers
+                x = np.clip(x + rng.normal(0, 3.0, len(x)), 0, 22500)
+                y = np.clip(y + rng.normal(0, 3.0, len(y)), 0, 22500)
+                d[1].copy_(T(x))
+                d[2].copy_(T(y))
+                qx, qy = x[qi], y[qi]
+                d[4].copy_(T(qx))
+                d[5].copy_(T(qy))
+            out = g.tick_device(*d, out=out)
+            torch.cuda.synchronize()
+            want = ref.process_tick(snap.ids, x, y, qi, qx, qy)
+            nres = out["n_results"]
+            assert np.array_equal(out["query_ids"].cpu().numpy(), want.query_ids), t
+            assert np.array_equal(out["offsets"].cpu().numpy(), want.offsets), t
+            assert np.array_equal(out["neighbour_ids"][:nres].cpu().numpy(), want.neighbour_ids), t
+            assert out["distances"][:nres].cpu().numpy().tobytes() == want.distances.tobytes(), t
+            for key in keys:
+                assert getattr(g.last_metrics, key) == getattr(ref.last_metrics, key), (t, key)
+        cap, rep = g.graph_stats
+        assert cap >= 1 and rep >= 3, (cap, rep)
+
+    # delta path: 10 % updates per tick re-index in full -> graph replays
+    with Engine(EngineConfig(k=k, region=synth.REGION)) as g, \
+            Engine(EngineConfig(k=k, region=synth.REGION)) as ref:
+        g.load(snap.ids, snap.x, snap.y)
+        x, y = snap.x.copy(), snap.y.copy()
+        qd = [T(a) for a in (qi, snap.x[qi], snap.y[qi])]
+        out = None
+        for t in range(6):
+            sel = rng.choice(len(x), len(x) // 10, replace=False)
+            ux = np.clip(x[sel] + rng.normal(0, 20.0, len(sel)), 0, 22500)
+            uy = np.clip(y[sel] + rng.normal(0, 20.0, len(sel)), 0, 22500)
+            x[sel], y[sel] = ux, uy
+            g.update(T(snap.ids[sel]), T(ux), T(uy))
+            out = g.query_device(*qd, out=out)
+            torch.cuda.synchronize()
+            want = ref.process_tick(snap.ids, x, y, qi, snap.x[qi], snap.y[qi])
+            nres = out["n_results"]
+            assert np.array_equal(out["neighbour_ids"][:nres].cpu().numpy(), want.neighbour_ids), t
+            assert out["distances"][:nres].cpu().numpy().tobytes() == want.distances.tobytes(), t
+            for key in keys:
+                assert getattr(g.last_metrics, key) == getattr(ref.last_metrics, key), (t, key)
+        cap, rep = g.graph_stats
+        assert rep >= 3, (cap, rep)
+
+
 def test_device_calls_follow_the_torch_stream():
     """Tensors produced on a side stream (async pinned copies, a sleep kernel
     ahead of them) feed update/query_device/tick_device on that stream: the
