@@ -1,6 +1,9 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q -x --durations=5 > gpurun_out/pytest_r2c.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_r2c.log
-tail -12 gpurun_out/pytest_r2c.log
-for wl in cfg2 cfg3; do
-  timeout 600 python bench.py --workload $wl --steps 20 --warmup 3 --e2e-steps 1 --no-cpu-baseline > gpurun_out/bg_$wl.json 2> gpurun_out/bg_$wl.err
-done
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
+bash tools/gpu_matrix.sh cfg2 cfg3 cfg3u k1 k8 k32 k128 cfg4 > gpurun_out/matrix.txt 2>&1
+timeout 900 python bench.py --steps 10 --warmup 3 --e2e-steps 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+   python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
+python tools/launch_summary.py gpurun_out/launches.csv 3 > gpurun_out/launches_cfg3.txt 2>&1
+bash tools/gpu_prof_r2.sh cfg3 cfg3u cfg2 k1 k8 k128 cfg4 > gpurun_out/prof.txt 2>&1
