@@ -228,6 +228,7 @@ struct mknn_engine {
   bool retry_radix = false;    // the redo of a tick sorts its issuers with the radix path
   int32_t h_l_deep = 0;
   int64_t h_n_leaves = 0, h_overfull = 0, h_n_build = 0, h_n_sub = 0;
+  int64_t h_bucket_load = 0;  // largest partition-bucket build load, 1/16 of the mean
   DevStore st;
   DevQueries dq;
 
@@ -412,6 +413,7 @@ int refresh_index_info(mknn_engine* h) {
   h->h_overfull = sc[2];
   h->h_n_build = sc[3];
   h->h_n_sub = sc[4];
+  h->h_bucket_load = sc[5];
   return 0;
 }
 
@@ -469,7 +471,8 @@ int graph_key(mknn_engine* h, int64_t n, const long long* ids, const double* x, 
           (uintptr_t)qx, (uintptr_t)qy, (uintptr_t)o.qids, (uintptr_t)o.len,
           (uintptr_t)o.offsets, (uintptr_t)o.nids, (uintptr_t)o.dist,
           (uintptr_t)h->scratch.p, (uintptr_t)h->pin, (uintptr_t)h->dq.bm_cap,
-          (uintptr_t)h->st.cap_sub, (uintptr_t)h->st.cap_box, (uintptr_t)(h->n_spec >= 0)};
+          (uintptr_t)h->st.cap_sub, (uintptr_t)h->st.cap_box, (uintptr_t)(h->n_spec >= 0),
+          (uintptr_t)h->h_bucket_load};
   for (void* b : engine_buffers(h)) key->push_back((uintptr_t)b);
   *ok = true;
   return 0;
@@ -592,7 +595,8 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
                                      cudaMemcpyDeviceToDevice, s));
       } else {
         if ((rc = store_index_objects(h->st, h->ix, h->r, ids, x, y, n, h->h_n_leaves, h->h_n_sub,
-                                      h->counters + 3, h->scratch.p, s)))
+                                      h->h_bucket_load <= 4 * 16, h->counters + 3, h->scratch.p,
+                                      s)))
           return h->set_err(rc);
         MKNN_CUDA_OK(cudaMemcpyAsync(h->clamped_total, h->counters + 3, sizeof(unsigned long long),
                                      cudaMemcpyDeviceToDevice, s));

@@ -18,6 +18,7 @@
 // not the reference's stable order; nothing observable depends on it because
 // selection is canonical in (d2, id) (see mknn_search.cu).
 #include <algorithm>
+#include <cstdlib>
 
 #include "mknn_internal.h"
 
@@ -200,7 +201,7 @@ __global__ void k_point_keys(const double* __restrict__ x, const double* __restr
         point_key(xi[u], yi[u], r, l_deep, info, leaf, key);
         if (leaf_out) leaf_out[i] = leaf;
         key_out[i] = key;
-        atomicAdd(&cnt[key], 1);
+        if (cnt) atomicAdd(&cnt[key], 1);
         if (bucket_cnt) atomicAdd(&bh[key >> bshift], 1);
       }
     }
@@ -308,6 +309,73 @@ __global__ void k_final_scatter(const StoreRec* __restrict__ rec, int64_t n,
 #pragma unroll
     for (int u = 0; u < U; u++)
       if (i0 + u * stride < n) st_rec(&obj[pos[u]], rc[u]);
+  }
+}
+
+// Pass 2, bucket-local: one CTA sorts one partition bucket by sub-cell key
+// in shared memory -- no global atomics.  The bucket's records occupy
+// [bstart[b], bstart[b + 1]) of the staging array, and exactly that range
+// of the store, so a sweep counts the bucket's keys into a shared histogram
+// (its 2^bshift keys), a block scan turns the counts into the keys' store
+// starts (written to kstart), and a second sweep places every record at its
+// key's start plus a shared-atomic rank.  CTAs walk the buckets in order so
+// the records of the second sweep are still in L2.
+constexpr int BS_THREADS = 1024;
+
+__global__ void __launch_bounds__(BS_THREADS, 1) k_bucket_sort(
+    const StoreRec* __restrict__ rec, const int32_t* __restrict__ bstart, int bshift,
+    int64_t n_sub, int64_t n, int32_t* __restrict__ kstart, StoreRec* __restrict__ obj) {
+  extern __shared__ int32_t hist[];  // 2^bshift
+  __shared__ int32_t wsum[BS_THREADS / 32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (blockIdx.x == 0 && t == 0) kstart[n_sub] = (int32_t)n;
+  for (int b = blockIdx.x; b < PT_BUCKETS; b += gridDim.x) {
+    const int64_t kb = (int64_t)b << bshift;
+    if (kb >= n_sub) break;
+    const int64_t kr = n_sub - kb, kw = (int64_t)1 << bshift;
+    const int nk = (int)(kr < kw ? kr : kw);
+    const int bs = bstart[b], be = bstart[b + 1];
+    for (int j = t; j < nk; j += BS_THREADS) hist[j] = 0;
+    __syncthreads();
+    for (int i = bs + t; i < be; i += BS_THREADS) atomicAdd(&hist[(int)(__ldg(&rec[i].key) - kb)], 1);
+    __syncthreads();
+    // exclusive scan of hist[0, nk): E contiguous entries per thread
+    const int E = (nk + BS_THREADS - 1) / BS_THREADS;
+    const int j0 = t * E, j1 = min(j0 + E, nk);
+    int sum = 0;
+    for (int j = j0; j < j1; j++) sum += hist[j];
+    int inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(FULL, inc, o);
+      if (lane >= o) inc += u;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+      const int v = wsum[lane];
+      int vi = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(FULL, vi, o);
+        if (lane >= o) vi += u;
+      }
+      wsum[lane] = vi - v;
+    }
+    __syncthreads();
+    int run = bs + wsum[w] + inc - sum;
+    for (int j = j0; j < j1; j++) {
+      const int c = hist[j];
+      hist[j] = run;
+      kstart[kb + j] = run;
+      run += c;
+    }
+    __syncthreads();
+    for (int i = bs + t; i < be; i += BS_THREADS) {
+      const StoreRec r = ld_rec(&rec[i]);
+      st_rec(&obj[atomicAdd(&hist[(int)(r.key - kb)], 1)], r);
+    }
+    __syncthreads();
   }
 }
 
@@ -522,6 +590,40 @@ __global__ void k_leaf_subs(const int32_t* __restrict__ build_counts,
   sub_size[l] = 1 << (2 * sl);
 }
 
+// rebuild: the build-time object load of each partition bucket (a leaf's
+// objects counted in the bucket of its first sub-cell key) -> scalars[5] =
+// the largest, in units of 1/16 of the mean; the bucket-local sort is used
+// only when no bucket is far above the mean (dense leaves whose sub-cells
+// are capped put many objects under few keys, and one CTA per bucket would
+// then serialise on them)
+__global__ void k_bucket_load(const int32_t* __restrict__ build_counts,
+                              const int32_t* __restrict__ sub_base, int32_t* __restrict__ scalars,
+                              int64_t ncap, uint32_t* __restrict__ load) {
+  const int64_t nl = scalars[1], n_sub = scalars[4];
+  int bshift = 0;
+  while (((n_sub > 1 ? n_sub : 1) - 1) >> bshift >= PT_BUCKETS) bshift++;
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < nl && l < ncap;
+       l += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&load[sub_base[l] >> bshift], (uint32_t)build_counts[l]);
+}
+
+__global__ void k_bucket_load_max(const uint32_t* __restrict__ load, int32_t* __restrict__ scalars) {
+  __shared__ uint32_t wmax[PT_BUCKETS / 32];
+  uint32_t v = load[threadIdx.x];
+  unsigned long long tot = v;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t m = 0;
+    for (int i = 0; i < PT_BUCKETS / 32; i++) m = max(m, wmax[i]);
+    const double mean = (double)max(scalars[3], 1) / PT_BUCKETS;
+    scalars[5] = (int32_t)min(16.0 * (double)m / mean, 1e9);
+  }
+  (void)tot;
+}
+
 __global__ void k_store_scalar(int32_t* scalars, const int32_t* __restrict__ src, int64_t idx) {
   scalars[4] = src[idx];
 }
@@ -619,6 +721,7 @@ int index_alloc(DevIndex& ix, int l_max, int th_quad) {
   MKNN_CUDA_OK(cudaMalloc(&ix.leaf_sub_bits, ncap));
   MKNN_CUDA_OK(cudaMalloc(&ix.leaf_sub_base, sizeof(int32_t) * (ncap + 1)));
   MKNN_CUDA_OK(cudaMalloc(&ix.cell_info, sizeof(unsigned long long) * ncap));
+  MKNN_CUDA_OK(cudaMalloc(&ix.bload, sizeof(uint32_t) * PT_BUCKETS));
   return 0;
 }
 
@@ -636,6 +739,7 @@ void index_free(DevIndex& ix) {
   cudaFree(ix.leaf_sub_bits);
   cudaFree(ix.leaf_sub_base);
   cudaFree(ix.cell_info);
+  cudaFree(ix.bload);
   ix = DevIndex{};
 }
 
@@ -683,6 +787,13 @@ int index_build(DevIndex& ix, const Region& r, const double* x, const double* y,
   // n_build for should_rebuild bookkeeping
   int32_t nb = (int32_t)std::min<int64_t>(n, 0x7fffffff);
   MKNN_CUDA_OK(cudaMemcpyAsync(ix.scalars + 3, &nb, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  // partition-bucket balance (scalars[5])
+  uint32_t* load = ix.bload;
+  MKNN_CUDA_OK(cudaMemsetAsync(load, 0, sizeof(uint32_t) * PT_BUCKETS, s));
+  MKNN_LAUNCH k_bucket_load<<<blocks_for(ncap), TPB, 0, s>>>(ix.build_counts, ix.leaf_sub_base,
+                                                             ix.scalars, ncap, load);
+  MKNN_LAUNCH k_bucket_load_max<<<1, PT_BUCKETS, 0, s>>>(load, ix.scalars);
+  MKNN_CUDA_OK(cudaGetLastError());
   return 0;
 }
 
@@ -745,14 +856,49 @@ static int store_finish(DevStore& st, const DevIndex& ix, int64_t n, int64_t n_l
 
 int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const long long* ids,
                         const double* x, const double* y, int64_t n, int64_t n_leaves,
-                        int64_t n_sub, unsigned long long* dev_clamped, void* scratch,
-                        cudaStream_t s) {
+                        int64_t n_sub, bool balanced, unsigned long long* dev_clamped,
+                        void* scratch, cudaStream_t s) {
+  // MKNN_BSORT=0: the global-atomic counting sort (per-key counts in the
+  // key pass, a scan over all sub-cells, an atomic final scatter) for A/B
+  static const bool bsort = [] {
+    const char* e = getenv("MKNN_BSORT");
+    return !(e && e[0] == '0');
+  }();
+  int bshift = 0;
+  while ((std::max<int64_t>(n_sub, 1) - 1) >> bshift >= PT_BUCKETS) bshift++;
+  if (bsort && bshift <= 14 && balanced) {  // <= 2^24 sub-cells: a 64 KB histogram
+    MKNN_CUDA_OK(cudaMemsetAsync(st.cursor, 0, sizeof(int32_t) * PT_BUCKETS, s));
+    if (n > 0)
+      MKNN_LAUNCH k_point_keys<<<grid_stride_blocks(n), TPB, 0, s>>>(
+          x, y, n, r, ix.scalars, ix.cell_info, nullptr, st.key, nullptr, dev_clamped, bshift,
+          st.cursor);
+    MKNN_CUDA_OK(cudaGetLastError());
+    MKNN_LAUNCH k_bucket_scan<<<1, PT_BUCKETS, 0, s>>>(st.cursor, st.bstart, st.cursor);
+    if (n > 0)
+      MKNN_LAUNCH k_partition<<<(unsigned)((n + PT_TILE - 1) / PT_TILE), PT_THREADS, 0, s>>>(
+          ids, x, y, st.key, n, bshift, st.cursor, st.rec);
+    MKNN_CUDA_OK(cudaGetLastError());
+    const size_t smem = sizeof(int32_t) << bshift;
+    static unsigned long long configured = 0;  // bit d: the attribute is set on device d
+    int dev = 0;
+    MKNN_CUDA_OK(cudaGetDevice(&dev));
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(__atomic_load_n(&configured, __ATOMIC_ACQUIRE) & bit)) {
+      MKNN_CUDA_OK(cudaFuncSetAttribute(k_bucket_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)(sizeof(int32_t) << 14)));
+      __atomic_fetch_or(&configured, bit, __ATOMIC_ACQ_REL);
+    }
+    int sms = 148;
+    MKNN_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    MKNN_LAUNCH k_bucket_sort<<<(unsigned)sms, BS_THREADS, smem, s>>>(st.rec, st.bstart, bshift,
+                                                                       n_sub, n, st.kstart, st.obj);
+    MKNN_CUDA_OK(cudaGetLastError());
+    return store_finish(st, ix, n, n_leaves, scratch, s);
+  }
   if (st.dirty) {
     MKNN_CUDA_OK(cudaMemsetAsync(st.cnt, 0, sizeof(int32_t) * st.cap_sub, s));
     st.dirty = false;
   }
-  int bshift = 0;
-  while ((std::max<int64_t>(n_sub, 1) - 1) >> bshift >= PT_BUCKETS) bshift++;
   MKNN_CUDA_OK(cudaMemsetAsync(st.cursor, 0, sizeof(int32_t) * PT_BUCKETS, s));
   if (n > 0)
     MKNN_LAUNCH k_point_keys<<<grid_stride_blocks(n), TPB, 0, s>>>(

@@ -58,12 +58,14 @@ struct DevIndex {
   uint32_t* leaf_key = nullptr;
   uint32_t* leaf_span = nullptr;
   int32_t* build_counts = nullptr;
-  int32_t* scalars = nullptr;  // [0] l_deep, [1] n_leaves, [2] overfull, [3] n_build, [4] n_sub
+  int32_t* scalars = nullptr;  // [0] l_deep, [1] n_leaves, [2] overfull, [3] n_build, [4] n_sub,
+                               // [5] largest partition-bucket build load (1/16 of the mean)
   // store ordering inside each leaf: 4^s sub-cells per leaf (s from the
   // leaf's build count), leaf l owns sub-cell keys [sub_base[l], sub_base[l+1])
   uint8_t* leaf_sub_bits = nullptr;  // 2*s
   int32_t* leaf_sub_base = nullptr;  // 4^l_max + 1
   unsigned long long* cell_info = nullptr;  // per deepest cell: sub_base | shift | bits | leaf
+  uint32_t* bload = nullptr;  // rebuild scratch: build load per partition bucket
   int l_max = 0;
   int th_quad = 0;
 };
@@ -161,10 +163,13 @@ int store_reserve(DevStore& st, int64_t n_sub, int64_t n_leaves, int64_t n);
 // dev_clamped (u64, device).  n_leaves / n_sub are host copies.
 // st.key[i] keeps every input index's key (the snapshot slot's key on the
 // delta path, which store_update_incremental maintains)
+// balanced: the partition buckets' build loads are near the mean (DevIndex
+// scalars[5]), so the bucket-local sort is used; otherwise the global-atomic
+// counting sort
 int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const long long* ids,
                         const double* x, const double* y, int64_t n, int64_t n_leaves,
-                        int64_t n_sub, unsigned long long* dev_clamped, void* scratch,
-                        cudaStream_t s);
+                        int64_t n_sub, bool balanced, unsigned long long* dev_clamped,
+                        void* scratch, cudaStream_t s);
 // Delta tick over the snapshot (sids/sx/sy, n_new slots): moved[0, m) are
 // the slots whose position changed (or were appended) since the store was
 // built from that snapshot.  dev_clamped_total: persistent count of objects

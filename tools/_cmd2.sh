@@ -1,2 +1,2 @@
-WLS="gaussian 1e7 1e6 32|uniform 1e7 1e6 32|uniform 1e6 1e5 32" VARS="MKNN_SELFCAP=0 MKNN_SELFCAP=1" bash tools/gpu_ab2.sh selfcap
-WLS="gaussian 1e7 1e6 128" VARS="MKNN_K128=0 MKNN_K128=1 MKNN_K128=2 MKNN_K128=3" bash tools/gpu_ab2.sh k128
+WLS="gaussian 1e7 1e6 32|uniform 1e7 1e6 32|uniform 1e6 1e5 32|uniform 1e8 1e7 16" VARS="MKNN_BSORT=0 MKNN_BSORT=1" bash tools/gpu_ab2.sh bsort2
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_bsort.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_bsort.log; tail -3 gpurun_out/pytest_bsort.log
