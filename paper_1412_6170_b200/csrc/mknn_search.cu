@@ -1071,10 +1071,16 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
   __syncwarp();
 
   // direction loop, left first (engine.py:645-681)
-  bool go_right = false;
+  // per query: left, right, left, ... (engine.py:645-681); a drained
+  // direction drops out.  Each lane keeps its own alternation, so a
+  // lane with one direction left navigates it every round instead of
+  // idling through the other direction's rounds (same per-query order)
+  bool next_right = false;
   if (a.debug_phase == 1) act_l = act_r = false;
   while (__any_sync(FULL, act_l || act_r)) {
-    const bool act = go_right ? act_r : act_l;
+    const bool go_right = (act_l && act_r) ? next_right : act_r;
+    const bool act = act_l || act_r;
+    next_right = !go_right;
     int li = -1;
     if (act) {
       int cur = go_right ? cur_r : cur_l;
@@ -1124,7 +1130,6 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
       if (lane == j) thr = kd;
     }
     __syncwarp();
-    go_right = !go_right;
   }
 
   // _emit: canonical order already; sqrt correctly rounded (engine.py:706)
@@ -1627,10 +1632,16 @@ __global__ void __launch_bounds__(32, MINB) k_search1(const __grid_constant__ Se
     }
 
     // direction loop, left first (engine.py:645-681)
-    bool go_right = false;
+    // per query: left, right, left, ... (engine.py:645-681); a drained
+    // direction drops out.  Each lane keeps its own alternation, so a
+    // lane with one direction left navigates it every round instead of
+    // idling through the other direction's rounds (same per-query order)
+    bool next_right = false;
     if (a.debug_phase == 1) act_l = act_r = false;
     while (__any_sync(FULL, act_l || act_r)) {
-      const bool act = go_right ? act_r : act_l;
+      const bool go_right = (act_l && act_r) ? next_right : act_r;
+      const bool act = act_l || act_r;
+      next_right = !go_right;
       int li = -1;
       if (act) {
         int cur = go_right ? cur_r : cur_l;
@@ -1667,7 +1678,6 @@ __global__ void __launch_bounds__(32, MINB) k_search1(const __grid_constant__ Se
         if (lane == j) thr = kd;
       }
       __syncwarp();
-      go_right = !go_right;
     }
 
     // _emit: canonical order already; sqrt correctly rounded (engine.py:706);

@@ -1,2 +1,2 @@
-WLS="gaussian 1e7 1e6 32|uniform 1e7 1e6 32|uniform 1e6 1e5 32|uniform 1e8 1e7 16" VARS="MKNN_BSORT=0 MKNN_BSORT=1" bash tools/gpu_ab2.sh bsort2
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_bsort.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_bsort.log; tail -3 gpurun_out/pytest_bsort.log
+WLS="gaussian 1e7 1e6 32|uniform 1e7 1e6 32|uniform 1e6 1e5 32|gaussian 1e7 1e6 8|gaussian 1e7 1e6 128" VARS="X=0" bash tools/gpu_ab2.sh lanealt
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_alt.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_alt.log; tail -3 gpurun_out/pytest_alt.log
