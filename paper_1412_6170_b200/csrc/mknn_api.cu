@@ -142,7 +142,7 @@ __global__ void k_update_apply(const long long* __restrict__ ids, const double* 
                                const double* __restrict__ y, int64_t nu,
                                const int32_t* __restrict__ slot_of, int32_t* winner,
                                long long* sids, double* sx, double* sy, int32_t* mark,
-                               int32_t epoch, int32_t* moved, int32_t* n_moved) {
+                               int32_t epoch, int32_t* moved, int32_t* n_moved, bool track) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nu;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t s = slot_of[i];
@@ -152,8 +152,9 @@ __global__ void k_update_apply(const long long* __restrict__ ids, const double* 
       sx[s] = x[i];
       sy[s] = y[i];
       // slots changed since the store was built (once per slot and epoch)
-      first = atomicExch(&mark[s], epoch) != epoch;
+      if (track) first = atomicExch(&mark[s], epoch) != epoch;
     }
+    if (!track) continue;
     // one counter atomic per warp (10M updates on one address serialise)
     const unsigned act = __activemask();
     const unsigned want = __ballot_sync(act, first);
@@ -280,6 +281,7 @@ struct mknn_engine {
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t gexec = nullptr;
   std::vector<uintptr_t> gkey;
+  std::vector<uintptr_t> gkey_seen;  // the previous graphable tick's key (capture on a repeat)
   int64_t graph_captures = 0, graph_replays = 0;
   long long graph_kernels = 0;  // kernel launches inside the captured graph
 
@@ -532,6 +534,12 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
   bool graphable = false;
   if ((rc = graph_key(h, n, ids, x, y, nq, qi, qx, qy, o, rebuild, sink, &gkey, &graphable)))
     return h->set_err(rc);
+  // capture only a shape seen on the previous graphable tick, so callers
+  // whose buffers change every tick never pay for captures
+  if (graphable && !(h->gexec && gkey == h->gkey) && gkey != h->gkey_seen) {
+    h->gkey_seen = gkey;
+    graphable = false;
+  }
   if (graphable && h->gexec && gkey == h->gkey) {
     MKNN_CUDA_OK(cudaGraphLaunch(h->gexec, s));
     note_launches(h->graph_kernels);
@@ -1140,9 +1148,15 @@ int snap_update_dev(mknn_engine* h, int64_t nu, const long long* ids, const doub
   cudaStream_t s = h->stream;
   MKNN_LAUNCH k_update_claim<<<gs_blocks(nu), 256, 0, s>>>(ids, nu, h->ht, (uint64_t)(h->hcap - 1),
                                                h->d_nsnap, h->winner, h->slot_of);
+  // a batch above the incremental threshold on its own (engine: > 5 % of
+  // the snapshot) sends the next tick to the full re-index anyway: skip the
+  // moved-slot bookkeeping (a random read-modify-write per update) and mark
+  // the store stale so the incremental path cannot be chosen on a partial list
+  const bool track = nu * 20 <= h->n_snap;
+  if (!track) h->st.valid = false;
   MKNN_LAUNCH k_update_apply<<<gs_blocks(nu), 256, 0, s>>>(ids, x, y, nu, h->slot_of, h->winner, h->snap_ids,
                                                h->snap_x, h->snap_y, h->mark, h->epoch, h->moved,
-                                               h->d_nmoved);
+                                               h->d_nmoved, track);
   MKNN_LAUNCH k_update_reset<<<gs_blocks(nu), 256, 0, s>>>(nu, h->slot_of, h->winner);
   MKNN_CUDA_OK(cudaGetLastError());
   h->upd_pending = true;
