@@ -230,6 +230,7 @@ struct mknn_engine {
   int32_t h_l_deep = 0;
   int64_t h_n_leaves = 0, h_overfull = 0, h_n_build = 0, h_n_sub = 0;
   int64_t h_bucket_load = 0;  // largest partition-bucket build load, 1/16 of the mean
+  int64_t h_bucket_keys = 0;  // largest partition-bucket key count
   DevStore st;
   DevQueries dq;
 
@@ -284,6 +285,7 @@ struct mknn_engine {
   std::vector<uintptr_t> gkey_seen;  // the previous graphable tick's key (capture on a repeat)
   int64_t graph_captures = 0, graph_replays = 0;
   long long graph_kernels = 0;  // kernel launches inside the captured graph
+  bool graph_dirty_after = false;  // the store's cnt-dirty flag after the captured sequence
 
   std::vector<int64_t> history;
   int64_t tick = 0;
@@ -361,7 +363,7 @@ int alloc_store(mknn_engine* h, int64_t n) {
     int64_t nc = std::max<int64_t>(n, h->st.cap * 3 / 2);
     void** old[] = {(void**)&h->st.obj, (void**)&h->st.rec, (void**)&h->st.key,
                     (void**)&h->st.rmflag, (void**)&h->st.rm_before, (void**)&h->st.mkey,
-                    (void**)&h->st.slot_pos, (void**)&h->st.deferred};
+                    (void**)&h->st.slot_pos, (void**)&h->st.deferred, (void**)&h->st.bkt};
     for (auto p : old) {
       cudaFree(*p);
       *p = nullptr;
@@ -375,6 +377,7 @@ int alloc_store(mknn_engine* h, int64_t n) {
     MKNN_CUDA_OK(cudaMalloc(&h->st.rm_before, sizeof(int32_t) * (nc + 2)));
     MKNN_CUDA_OK(cudaMalloc(&h->st.mkey, sizeof(uint32_t) * nc));
     MKNN_CUDA_OK(cudaMalloc(&h->st.slot_pos, sizeof(int32_t) * nc));
+    MKNN_CUDA_OK(cudaMalloc(&h->st.bkt, sizeof(uint16_t) * nc));
     MKNN_CUDA_OK(cudaMalloc(&h->st.deferred, sizeof(int32_t) * nc));
     if (!h->st.n_deferred) MKNN_CUDA_OK(cudaMalloc(&h->st.n_deferred, sizeof(int32_t)));
     h->st.cap = nc;
@@ -416,6 +419,7 @@ int refresh_index_info(mknn_engine* h) {
   h->h_n_build = sc[3];
   h->h_n_sub = sc[4];
   h->h_bucket_load = sc[5];
+  h->h_bucket_keys = sc[6];
   return 0;
 }
 
@@ -436,7 +440,7 @@ std::vector<void*> engine_buffers(mknn_engine* h) {
           h->up_ids, h->up_x, h->up_y, h->tk, h->tk_alt, h->tk_cnt, h->tv, h->tv_alt, h->prof,
           h->mark, h->moved, h->d_nmoved, h->clamped_total, h->work, h->st.kstart_alt,
           h->st.fill, h->st.qcnt, h->st.qkstart, h->st.rmflag, h->st.rm_before, h->st.mkey,
-          h->own_pos, h->own_thr, h->st.slot_pos, h->st.deferred, h->st.n_deferred};
+          h->own_pos, h->own_thr, h->st.slot_pos, h->st.deferred, h->st.n_deferred, h->st.bkt};
 }
 
 // A tick whose enqueue sequence is a pure function of the key below can run
@@ -474,7 +478,7 @@ int graph_key(mknn_engine* h, int64_t n, const long long* ids, const double* x, 
           (uintptr_t)o.offsets, (uintptr_t)o.nids, (uintptr_t)o.dist,
           (uintptr_t)h->scratch.p, (uintptr_t)h->pin, (uintptr_t)h->dq.bm_cap,
           (uintptr_t)h->st.cap_sub, (uintptr_t)h->st.cap_box, (uintptr_t)(h->n_spec >= 0),
-          (uintptr_t)h->h_bucket_load};
+          (uintptr_t)h->h_bucket_load, (uintptr_t)h->h_bucket_keys};
   for (void* b : engine_buffers(h)) key->push_back((uintptr_t)b);
   *ok = true;
   return 0;
@@ -546,7 +550,7 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
     // the host-side effects of the captured sequence (full re-index path)
     const bool from_snap = ids == h->snap_ids && x == h->snap_x && y == h->snap_y;
     h->last_tick_ok = false;
-    h->st.dirty = false;
+    h->st.dirty = h->graph_dirty_after;
     h->st.n_store = n;
     h->st.valid = from_snap;
     if (from_snap) {
@@ -603,7 +607,8 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
                                      cudaMemcpyDeviceToDevice, s));
       } else {
         if ((rc = store_index_objects(h->st, h->ix, h->r, ids, x, y, n, h->h_n_leaves, h->h_n_sub,
-                                      h->h_bucket_load <= 4 * 16, h->counters + 3, h->scratch.p,
+                                      h->h_bucket_load <= 4 * 16 && h->h_bucket_keys <= 16384,
+                                      h->counters + 3, h->scratch.p,
                                       s)))
           return h->set_err(rc);
         MKNN_CUDA_OK(cudaMemcpyAsync(h->clamped_total, h->counters + 3, sizeof(unsigned long long),
@@ -786,6 +791,7 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
       MKNN_CUDA_OK(ie);
       h->gkey = gkey;
       h->graph_kernels = launch_count() - launches0;
+      h->graph_dirty_after = h->st.dirty;
       MKNN_CUDA_OK(cudaGraphLaunch(h->gexec, s));
       h->graph_captures++;
     } else if (erc) {

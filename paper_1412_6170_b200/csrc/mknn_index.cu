@@ -171,7 +171,9 @@ __global__ void k_point_keys(const double* __restrict__ x, const double* __restr
                              uint32_t* __restrict__ leaf_out,
                              uint32_t* __restrict__ key_out, int32_t* __restrict__ cnt,
                              unsigned long long* clamped, int bshift,
-                             int32_t* __restrict__ bucket_cnt) {
+                             int32_t* __restrict__ bucket_cnt,
+                             const uint16_t* __restrict__ leaf_bucket = nullptr,
+                             uint16_t* __restrict__ bkt_out = nullptr) {
   // every key is counted in cnt; bucket_cnt != nullptr also counts the coarse
   // buckets (key >> bshift) of the store partition through a block histogram
   __shared__ int bh[PT_BUCKETS];
@@ -202,7 +204,14 @@ __global__ void k_point_keys(const double* __restrict__ x, const double* __restr
         if (leaf_out) leaf_out[i] = leaf;
         key_out[i] = key;
         if (cnt) atomicAdd(&cnt[key], 1);
-        if (bucket_cnt) atomicAdd(&bh[key >> bshift], 1);
+        if (bucket_cnt) {
+          int b = (int)(key >> bshift);
+          if (leaf_bucket) {
+            b = __ldg(&leaf_bucket[leaf]);
+            bkt_out[i] = (uint16_t)b;
+          }
+          atomicAdd(&bh[b], 1);
+        }
       }
     }
   }
@@ -256,18 +265,22 @@ __global__ void k_bucket_scan(const int32_t* __restrict__ bucket_cnt, int32_t* _
 __global__ void __launch_bounds__(PT_THREADS) k_partition(
     const long long* __restrict__ ids, const double* __restrict__ x, const double* __restrict__ y,
     const uint32_t* __restrict__ key, int64_t n, int bshift, int32_t* __restrict__ cursor,
-    StoreRec* __restrict__ out) {
+    StoreRec* __restrict__ out, const uint16_t* __restrict__ bkt = nullptr) {
+  // bkt: the leaf-aligned bucket of every object (k_point_keys); otherwise
+  // bucket = key >> bshift
   __shared__ int hist[PT_BUCKETS], gbase[PT_BUCKETS];
   const int t = threadIdx.x;
   const int64_t base = (int64_t)blockIdx.x * PT_TILE;
   const int tile_n = (n - base) < PT_TILE ? (int)(n - base) : PT_TILE;
   for (int i = t; i < PT_BUCKETS; i += PT_THREADS) hist[i] = 0;
   StoreRec rc[PT_ITEMS];
+  int bk[PT_ITEMS];
 #pragma unroll
   for (int j = 0; j < PT_ITEMS; j++) {
     const int li = t + j * PT_THREADS;
     if (li < tile_n) {
       const int64_t i = base + li;
+      bk[j] = bkt ? (int)bkt[i] : (int)(key[i] >> bshift);
       rc[j].key = key[i];
       rc[j].x = x[i];
       rc[j].y = y[i];
@@ -279,14 +292,14 @@ __global__ void __launch_bounds__(PT_THREADS) k_partition(
   int rank[PT_ITEMS];
 #pragma unroll
   for (int j = 0; j < PT_ITEMS; j++)
-    if (t + j * PT_THREADS < tile_n) rank[j] = atomicAdd(&hist[rc[j].key >> bshift], 1);
+    if (t + j * PT_THREADS < tile_n) rank[j] = atomicAdd(&hist[bk[j]], 1);
   __syncthreads();
   for (int i = t; i < PT_BUCKETS; i += PT_THREADS)
     if (hist[i]) gbase[i] = atomicAdd(&cursor[i], hist[i]);
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < PT_ITEMS; j++)
-    if (t + j * PT_THREADS < tile_n) st_rec(&out[gbase[rc[j].key >> bshift] + rank[j]], rc[j]);
+    if (t + j * PT_THREADS < tile_n) st_rec(&out[gbase[bk[j]] + rank[j]], rc[j]);
 }
 
 // Pass 2: final counting-sort scatter, reading the partitioned records in
@@ -321,19 +334,19 @@ __global__ void k_final_scatter(const StoreRec* __restrict__ rec, int64_t n,
 // key's start plus a shared-atomic rank.  CTAs walk the buckets in order so
 // the records of the second sweep are still in L2.
 constexpr int BS_THREADS = 1024;
+constexpr int BS_MAX_KEYS = 16384;  // 64 KB shared histogram
 
 __global__ void __launch_bounds__(BS_THREADS, 1) k_bucket_sort(
-    const StoreRec* __restrict__ rec, const int32_t* __restrict__ bstart, int bshift,
-    int64_t n_sub, int64_t n, int32_t* __restrict__ kstart, StoreRec* __restrict__ obj) {
+    const StoreRec* __restrict__ rec, const int32_t* __restrict__ bstart,
+    const int32_t* __restrict__ bkey, int64_t n_sub, int64_t n, int32_t* __restrict__ kstart,
+    StoreRec* __restrict__ obj) {
   extern __shared__ int32_t hist[];  // 2^bshift
   __shared__ int32_t wsum[BS_THREADS / 32];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   if (blockIdx.x == 0 && t == 0) kstart[n_sub] = (int32_t)n;
   for (int b = blockIdx.x; b < PT_BUCKETS; b += gridDim.x) {
-    const int64_t kb = (int64_t)b << bshift;
-    if (kb >= n_sub) break;
-    const int64_t kr = n_sub - kb, kw = (int64_t)1 << bshift;
-    const int nk = (int)(kr < kw ? kr : kw);
+    const int64_t kb = bkey[b];
+    const int nk = bkey[b + 1] - bkey[b];  // <= BS_MAX_KEYS (checked at the rebuild)
     const int bs = bstart[b], be = bstart[b + 1];
     for (int j = t; j < nk; j += BS_THREADS) hist[j] = 0;
     __syncthreads();
@@ -590,27 +603,59 @@ __global__ void k_leaf_subs(const int32_t* __restrict__ build_counts,
   sub_size[l] = 1 << (2 * sl);
 }
 
-// rebuild: the build-time object load of each partition bucket (a leaf's
-// objects counted in the bucket of its first sub-cell key) -> scalars[5] =
-// the largest, in units of 1/16 of the mean; the bucket-local sort is used
-// only when no bucket is far above the mean (dense leaves whose sub-cells
-// are capped put many objects under few keys, and one CTA per bucket would
-// then serialise on them)
-__global__ void k_bucket_load(const int32_t* __restrict__ build_counts,
-                              const int32_t* __restrict__ sub_base, int32_t* __restrict__ scalars,
-                              int64_t ncap, uint32_t* __restrict__ load) {
+// rebuild: partition buckets for the bucket-local store sort, aligned to
+// leaves and balanced by the build counts -- leaf l goes to bucket
+// floor(objects before l * NB / n_build), bucket b holds the keys
+// [bkey[b], bkey[b + 1]) -- so a dense leaf whose sub-cells are capped does
+// not pile its objects into one bucket.  pre: exclusive scan of the build
+// counts (0 past the last leaf)
+__global__ void k_leaf_bucket(const int32_t* __restrict__ pre, const int32_t* __restrict__ sub_base,
+                              const int32_t* __restrict__ scalars, int64_t ncap,
+                              uint16_t* __restrict__ leaf_bucket, int32_t* __restrict__ bkey) {
   const int64_t nl = scalars[1], n_sub = scalars[4];
-  int bshift = 0;
-  while (((n_sub > 1 ? n_sub : 1) - 1) >> bshift >= PT_BUCKETS) bshift++;
+  const int64_t nb = scalars[3] > 0 ? scalars[3] : 1;
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l <= nl && l < ncap + 1;
+       l += (int64_t)gridDim.x * blockDim.x) {
+    const int b = l < nl ? (int)min((int64_t)pre[l] * PT_BUCKETS / nb, (int64_t)PT_BUCKETS - 1)
+                         : PT_BUCKETS;
+    const int bp = l == 0 ? -1 : (int)min((int64_t)pre[l - 1] * PT_BUCKETS / nb, (int64_t)PT_BUCKETS - 1);
+    if (l < nl) leaf_bucket[l] = (uint16_t)b;
+    const int32_t k0 = l < nl ? sub_base[l] : (int32_t)n_sub;
+    for (int bb = bp + 1; bb <= b; bb++) bkey[bb] = k0;  // buckets this leaf opens
+  }
+}
+
+// the largest key count of a bucket -> scalars[6] (the bucket-local sort
+// keeps a bucket's key histogram in shared memory)
+__global__ void k_bucket_keys(const int32_t* __restrict__ bkey, int32_t* __restrict__ scalars) {
+  __shared__ int wk[PT_BUCKETS / 32];
+  const int b = threadIdx.x;
+  int mk = bkey[b + 1] - bkey[b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mk = max(mk, __shfl_xor_sync(FULL, mk, o));
+  if ((b & 31) == 0) wk[b >> 5] = mk;
+  __syncthreads();
+  if (b == 0) {
+    int m = 0;
+    for (int i = 0; i < PT_BUCKETS / 32; i++) m = max(m, wk[i]);
+    scalars[6] = m;
+  }
+}
+
+// the build load of every bucket -> scalars[5] (largest, 1/16 of the mean)
+__global__ void k_bucket_load(const int32_t* __restrict__ build_counts,
+                              const uint16_t* __restrict__ leaf_bucket,
+                              const int32_t* __restrict__ scalars, int64_t ncap,
+                              uint32_t* __restrict__ load) {
+  const int64_t nl = scalars[1];
   for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < nl && l < ncap;
        l += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(&load[sub_base[l] >> bshift], (uint32_t)build_counts[l]);
+    atomicAdd(&load[leaf_bucket[l]], (uint32_t)build_counts[l]);
 }
 
 __global__ void k_bucket_load_max(const uint32_t* __restrict__ load, int32_t* __restrict__ scalars) {
   __shared__ uint32_t wmax[PT_BUCKETS / 32];
   uint32_t v = load[threadIdx.x];
-  unsigned long long tot = v;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
   if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = v;
@@ -621,7 +666,14 @@ __global__ void k_bucket_load_max(const uint32_t* __restrict__ load, int32_t* __
     const double mean = (double)max(scalars[3], 1) / PT_BUCKETS;
     scalars[5] = (int32_t)min(16.0 * (double)m / mean, 1e9);
   }
-  (void)tot;
+}
+
+// build counts of the leaves, 0 past the last one (the scan input)
+__global__ void k_leaf_counts(const int32_t* __restrict__ build_counts,
+                              const int32_t* __restrict__ scalars, int64_t ncap,
+                              int32_t* __restrict__ out) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l < ncap) out[l] = l < scalars[1] ? build_counts[l] : 0;
 }
 
 __global__ void k_store_scalar(int32_t* scalars, const int32_t* __restrict__ src, int64_t idx) {
@@ -722,6 +774,8 @@ int index_alloc(DevIndex& ix, int l_max, int th_quad) {
   MKNN_CUDA_OK(cudaMalloc(&ix.leaf_sub_base, sizeof(int32_t) * (ncap + 1)));
   MKNN_CUDA_OK(cudaMalloc(&ix.cell_info, sizeof(unsigned long long) * ncap));
   MKNN_CUDA_OK(cudaMalloc(&ix.bload, sizeof(uint32_t) * PT_BUCKETS));
+  MKNN_CUDA_OK(cudaMalloc(&ix.bkey, sizeof(int32_t) * (PT_BUCKETS + 1)));
+  MKNN_CUDA_OK(cudaMalloc(&ix.leaf_bucket, sizeof(uint16_t) * ncap));
   return 0;
 }
 
@@ -740,6 +794,8 @@ void index_free(DevIndex& ix) {
   cudaFree(ix.leaf_sub_base);
   cudaFree(ix.cell_info);
   cudaFree(ix.bload);
+  cudaFree(ix.bkey);
+  cudaFree(ix.leaf_bucket);
   ix = DevIndex{};
 }
 
@@ -787,12 +843,21 @@ int index_build(DevIndex& ix, const Region& r, const double* x, const double* y,
   // n_build for should_rebuild bookkeeping
   int32_t nb = (int32_t)std::min<int64_t>(n, 0x7fffffff);
   MKNN_CUDA_OK(cudaMemcpyAsync(ix.scalars + 3, &nb, sizeof(int32_t), cudaMemcpyHostToDevice, s));
-  // partition-bucket balance (scalars[5])
-  uint32_t* load = ix.bload;
-  MKNN_CUDA_OK(cudaMemsetAsync(load, 0, sizeof(uint32_t) * PT_BUCKETS, s));
-  MKNN_LAUNCH k_bucket_load<<<blocks_for(ncap), TPB, 0, s>>>(ix.build_counts, ix.leaf_sub_base,
-                                                             ix.scalars, ncap, load);
-  MKNN_LAUNCH k_bucket_load_max<<<1, PT_BUCKETS, 0, s>>>(load, ix.scalars);
+  // leaf-aligned, load-balanced partition buckets (bucket-local sort) and
+  // their balance (scalars[5], [6]); scratch: flags (the scan is done)
+  int32_t* lc = flags;
+  int32_t* pre = flags + ncap + 1;
+  MKNN_LAUNCH k_leaf_counts<<<blocks_for(ncap), TPB, 0, s>>>(ix.build_counts, ix.scalars, ncap, lc);
+  MKNN_CUDA_OK(cudaGetLastError());
+  rc = exclusive_scan_i32(lc, pre, ncap, scratch, s);
+  if (rc) return rc;
+  MKNN_LAUNCH k_leaf_bucket<<<blocks_for(ncap + 1), TPB, 0, s>>>(pre, ix.leaf_sub_base, ix.scalars, ncap,
+                                                                ix.leaf_bucket, ix.bkey);
+  MKNN_CUDA_OK(cudaMemsetAsync(ix.bload, 0, sizeof(uint32_t) * PT_BUCKETS, s));
+  MKNN_LAUNCH k_bucket_load<<<blocks_for(ncap), TPB, 0, s>>>(ix.build_counts, ix.leaf_bucket,
+                                                             ix.scalars, ncap, ix.bload);
+  MKNN_LAUNCH k_bucket_load_max<<<1, PT_BUCKETS, 0, s>>>(ix.bload, ix.scalars);
+  MKNN_LAUNCH k_bucket_keys<<<1, PT_BUCKETS, 0, s>>>(ix.bkey, ix.scalars);
   MKNN_CUDA_OK(cudaGetLastError());
   return 0;
 }
@@ -868,19 +933,19 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
   while ((std::max<int64_t>(n_sub, 1) - 1) >> bshift >= PT_BUCKETS) bshift++;
   // <= 2^24 sub-cells: a 64 KB histogram; buckets of <= 32K records (1 MB)
   // so the second sweep still finds them in L2 (100M objects: 6.20 -> 6.32 ms)
-  if (bsort && bshift <= 14 && balanced && n <= (int64_t)PT_BUCKETS * 32768) {
+  if (bsort && balanced && n <= (int64_t)PT_BUCKETS * 32768) {
     MKNN_CUDA_OK(cudaMemsetAsync(st.cursor, 0, sizeof(int32_t) * PT_BUCKETS, s));
     if (n > 0)
       MKNN_LAUNCH k_point_keys<<<grid_stride_blocks(n), TPB, 0, s>>>(
           x, y, n, r, ix.scalars, ix.cell_info, nullptr, st.key, nullptr, dev_clamped, bshift,
-          st.cursor);
+          st.cursor, ix.leaf_bucket, st.bkt);
     MKNN_CUDA_OK(cudaGetLastError());
     MKNN_LAUNCH k_bucket_scan<<<1, PT_BUCKETS, 0, s>>>(st.cursor, st.bstart, st.cursor);
     if (n > 0)
       MKNN_LAUNCH k_partition<<<(unsigned)((n + PT_TILE - 1) / PT_TILE), PT_THREADS, 0, s>>>(
-          ids, x, y, st.key, n, bshift, st.cursor, st.rec);
+          ids, x, y, st.key, n, bshift, st.cursor, st.rec, st.bkt);
     MKNN_CUDA_OK(cudaGetLastError());
-    const size_t smem = sizeof(int32_t) << bshift;
+    const size_t smem = sizeof(int32_t) * BS_MAX_KEYS;
     static unsigned long long configured = 0;  // bit d: the attribute is set on device d
     int dev = 0;
     MKNN_CUDA_OK(cudaGetDevice(&dev));
@@ -892,7 +957,7 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
     }
     int sms = 148;
     MKNN_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    MKNN_LAUNCH k_bucket_sort<<<(unsigned)sms, BS_THREADS, smem, s>>>(st.rec, st.bstart, bshift,
+    MKNN_LAUNCH k_bucket_sort<<<(unsigned)sms, BS_THREADS, smem, s>>>(st.rec, st.bstart, ix.bkey,
                                                                        n_sub, n, st.kstart, st.obj);
     MKNN_CUDA_OK(cudaGetLastError());
     return store_finish(st, ix, n, n_leaves, scratch, s);

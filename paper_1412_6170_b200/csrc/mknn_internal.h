@@ -59,13 +59,16 @@ struct DevIndex {
   uint32_t* leaf_span = nullptr;
   int32_t* build_counts = nullptr;
   int32_t* scalars = nullptr;  // [0] l_deep, [1] n_leaves, [2] overfull, [3] n_build, [4] n_sub,
-                               // [5] largest partition-bucket build load (1/16 of the mean)
+                               // [5] largest partition-bucket build load (1/16 of the mean),
+                               // [6] largest partition-bucket key count
   // store ordering inside each leaf: 4^s sub-cells per leaf (s from the
   // leaf's build count), leaf l owns sub-cell keys [sub_base[l], sub_base[l+1])
   uint8_t* leaf_sub_bits = nullptr;  // 2*s
   int32_t* leaf_sub_base = nullptr;  // 4^l_max + 1
   unsigned long long* cell_info = nullptr;  // per deepest cell: sub_base | shift | bits | leaf
   uint32_t* bload = nullptr;  // rebuild scratch: build load per partition bucket
+  int32_t* bkey = nullptr;       // leaf-aligned partition buckets: bucket b = keys [bkey[b], bkey[b+1])
+  uint16_t* leaf_bucket = nullptr;  // bucket of every leaf
   int l_max = 0;
   int th_quad = 0;
 };
@@ -126,6 +129,7 @@ struct DevStore {
   StoreRec* obj = nullptr;        // leaf-sorted objects
   StoreRec* rec = nullptr;        // staging of the bucket partition pass
   uint32_t* key = nullptr;        // sub-cell key per input object / query
+  uint16_t* bkt = nullptr;        // partition bucket per input object (bucket-local sort)
   int64_t cap = 0;
   int32_t* cell_start = nullptr;  // 4^l_max + 2 (start[L] = n)
   int32_t* chunk_start = nullptr; // 4^l_max + 2 (chunk ordinal of each leaf's first chunk)
