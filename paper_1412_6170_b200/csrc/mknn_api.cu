@@ -430,7 +430,7 @@ int validate_counts(mknn_engine* h, int64_t n, int64_t nq);
 // Every device buffer the engine owns (destroy frees them; a graph key
 // includes them, so any reallocation forces a new capture).
 std::vector<void*> engine_buffers(mknn_engine* h) {
-  return {h->st.obj, h->st.rec, h->st.cursor, h->st.bstart, h->st.key, h->st.cell_start,
+  return {h->st.obj, h->st.rec, h->st.cursor, h->st.bstart, h->st.cbase, h->st.key, h->st.cell_start,
           h->st.chunk_start, h->st.nch, h->st.box, h->st.crange, h->st.cnt, h->st.kstart,
           h->dq.leaf, h->dq.qkey, h->dq.order, h->dq.row, h->dq.keys, h->dq.keys_alt, h->dq.vals,
           h->dq.vals_alt, h->dq.minmax, h->dq.bm, h->dq.bm_cnt, h->dq.bm_pre, h->dq.dup,

@@ -334,62 +334,165 @@ __global__ void k_final_scatter(const StoreRec* __restrict__ rec, int64_t n,
 // key's start plus a shared-atomic rank.  CTAs walk the buckets in order so
 // the records of the second sweep are still in L2.
 constexpr int BS_THREADS = 1024;
-constexpr int BS_MAX_KEYS = 16384;  // 64 KB shared histogram
+constexpr int BS_MAX_KEYS = 16384;  // 64 KB shared histogram (and <= that many leaves per bucket)
 
+// in-place exclusive scan of v[0, m) by the whole CTA, plus `base`;
+// returns the total (v[m] is not written)
+__device__ __forceinline__ int block_exclusive_scan(int32_t* v, int m, int base, int32_t* wsum) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int E = (m + BS_THREADS - 1) / BS_THREADS;
+  const int j0 = min(t * E, m), j1 = min(j0 + E, m);
+  int sum = 0;
+  for (int j = j0; j < j1; j++) sum += v[j];
+  int inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const int x = wsum[lane];
+    int xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(FULL, xi, o);
+      if (lane >= o) xi += u;
+    }
+    wsum[lane] = xi - x;
+    if (lane == 31) wsum[BS_THREADS / 32] = xi;  // the total
+  }
+  __syncthreads();
+  int run = base + wsum[w] + inc - sum;
+  for (int j = j0; j < j1; j++) {
+    const int c = v[j];
+    v[j] = run;
+    run += c;
+  }
+  const int total = wsum[BS_THREADS / 32];
+  __syncthreads();
+  return total;
+}
+
+struct BucketLeaves {  // the leaf side of k_bucket_sort (store_finish's passes, fused)
+  const int32_t* leaf_first;  // [NB + 1]: bucket b holds leaves [leaf_first[b], leaf_first[b + 1])
+  const int32_t* sub_base;    // leaf -> its first sub-cell key
+  const int32_t* cbase;       // [NB]: first chunk slot of bucket b
+  int32_t* cell_start;        // out, per leaf (+ [n_leaves] = n)
+  int32_t* chunk_start;       // out, per leaf (slots are sparse: c1 = c0 + chunks of the leaf)
+  ChunkBox* box;              // out, per chunk slot
+  int chunk;                  // objects per chunk
+  int64_t n_leaves;
+};
+
+// Pass 2, bucket-local: one CTA sorts one partition bucket by sub-cell key
+// in shared memory -- no global atomics.  The bucket's records occupy
+// [bstart[b], bstart[b + 1]) of the staging array, and exactly that range
+// of the store, so a sweep counts the bucket's keys [bkey[b], bkey[b + 1])
+// into a shared histogram, a block scan turns the counts into the keys'
+// store starts (written to kstart), and a second sweep places every record
+// at its key's start plus a shared-atomic rank.  Buckets are whole leaves,
+// so the CTA then derives its leaves' ranges and chunks and computes the
+// chunk boxes from the records it just placed (still in L2): no separate
+// leaf-range, chunk-range and box passes over the store.  CTAs walk the
+// buckets in order so the second sweep finds its bucket in L2.
 __global__ void __launch_bounds__(BS_THREADS, 1) k_bucket_sort(
     const StoreRec* __restrict__ rec, const int32_t* __restrict__ bstart,
     const int32_t* __restrict__ bkey, int64_t n_sub, int64_t n, int32_t* __restrict__ kstart,
-    StoreRec* __restrict__ obj) {
-  extern __shared__ int32_t hist[];  // 2^bshift
-  __shared__ int32_t wsum[BS_THREADS / 32];
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  if (blockIdx.x == 0 && t == 0) kstart[n_sub] = (int32_t)n;
+    StoreRec* __restrict__ obj, const BucketLeaves bl) {
+  extern __shared__ int32_t sm[];
+  int32_t* hist = sm;                   // BS_MAX_KEYS: key counts, then starts, then ends
+  int32_t* lpre = sm + BS_MAX_KEYS;     // BS_MAX_KEYS + 1: chunks per leaf, then their prefix
+  int32_t* lcs = sm + 2 * BS_MAX_KEYS + 1;  // BS_MAX_KEYS: leaf range starts
+  __shared__ int32_t wsum[BS_THREADS / 32 + 1];
+  const int t = threadIdx.x;
+  if (blockIdx.x == 0 && t == 0) {
+    kstart[n_sub] = (int32_t)n;
+    bl.cell_start[bl.n_leaves] = (int32_t)n;
+  }
   for (int b = blockIdx.x; b < PT_BUCKETS; b += gridDim.x) {
-    const int64_t kb = bkey[b];
-    const int nk = bkey[b + 1] - bkey[b];  // <= BS_MAX_KEYS (checked at the rebuild)
+    const int kb = bkey[b];
+    const int nk = bkey[b + 1] - kb;  // <= BS_MAX_KEYS (checked at the rebuild)
     const int bs = bstart[b], be = bstart[b + 1];
     for (int j = t; j < nk; j += BS_THREADS) hist[j] = 0;
     __syncthreads();
-    for (int i = bs + t; i < be; i += BS_THREADS) atomicAdd(&hist[(int)(__ldg(&rec[i].key) - kb)], 1);
+    for (int i = bs + t; i < be; i += BS_THREADS) atomicAdd(&hist[(int)__ldg(&rec[i].key) - kb], 1);
     __syncthreads();
-    // exclusive scan of hist[0, nk): E contiguous entries per thread
-    const int E = (nk + BS_THREADS - 1) / BS_THREADS;
-    const int j0 = t * E, j1 = min(j0 + E, nk);
-    int sum = 0;
-    for (int j = j0; j < j1; j++) sum += hist[j];
-    int inc = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int u = __shfl_up_sync(FULL, inc, o);
-      if (lane >= o) inc += u;
-    }
-    if (lane == 31) wsum[w] = inc;
-    __syncthreads();
-    if (w == 0) {
-      const int v = wsum[lane];
-      int vi = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(FULL, vi, o);
-        if (lane >= o) vi += u;
-      }
-      wsum[lane] = vi - v;
-    }
-    __syncthreads();
-    int run = bs + wsum[w] + inc - sum;
-    for (int j = j0; j < j1; j++) {
-      const int c = hist[j];
-      hist[j] = run;
-      kstart[kb + j] = run;
-      run += c;
-    }
+    block_exclusive_scan(hist, nk, bs, wsum);
+    for (int j = t; j < nk; j += BS_THREADS) kstart[kb + j] = hist[j];
     __syncthreads();
     for (int i = bs + t; i < be; i += BS_THREADS) {
       const StoreRec r = ld_rec(&rec[i]);
-      st_rec(&obj[atomicAdd(&hist[(int)(r.key - kb)], 1)], r);
+      st_rec(&obj[atomicAdd(&hist[(int)r.key - kb], 1)], r);
+    }
+    __syncthreads();
+    // hist[j] is now the end of key j: a leaf starts where its first key does
+    const int lf = bl.leaf_first[b], nlb = bl.leaf_first[b + 1] - lf;  // <= nk
+    for (int l = t; l < nlb; l += BS_THREADS) {
+      const int k0 = bl.sub_base[lf + l] - kb, k1 = bl.sub_base[lf + l + 1] - kb;
+      const int cs = k0 == 0 ? bs : hist[k0 - 1];
+      const int ce = k1 == 0 ? bs : hist[k1 - 1];
+      lcs[l] = cs;
+      lpre[l] = (ce - cs + bl.chunk - 1) / bl.chunk;
+      bl.cell_start[lf + l] = cs;
+    }
+    __syncthreads();
+    const int nchunks = block_exclusive_scan(lpre, nlb, 0, wsum);
+    const int cb = bl.cbase[b];
+    for (int l = t; l < nlb; l += BS_THREADS) bl.chunk_start[lf + l] = cb + lpre[l];
+    if (t == 0) lpre[nlb] = nchunks;
+    __syncthreads();
+    for (int q = t; q < nchunks; q += BS_THREADS) {
+      int lo = 0, hi = nlb;  // the leaf: lpre[lo] <= q < lpre[lo + 1]
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (lpre[mid] <= q) lo = mid; else hi = mid;
+      }
+      const int o0 = lcs[lo] + (q - lpre[lo]) * bl.chunk;
+      const int oe = lo + 1 < nlb ? lcs[lo + 1] : be;
+      const int o1 = min(o0 + bl.chunk, oe);
+      double xl = DINF, yl = DINF, xh = -DINF, yh = -DINF;
+      for (int o = o0; o < o1; o++) {
+        const double2 p = *reinterpret_cast<const double2*>(&obj[o]);
+        xl = fmin(xl, p.x);
+        xh = fmax(xh, p.x);
+        yl = fmin(yl, p.y);
+        yh = fmax(yh, p.y);
+      }
+      bl.box[cb + q] = ChunkBox{xl, yl, xh, yh};
     }
     __syncthreads();
   }
+}
+
+// chunk slot bases of the buckets: an upper bound of each bucket's chunks
+// (ceil(objects / chunk) + its leaves), scanned (one CTA of PT_BUCKETS)
+__global__ void k_chunk_base(const int32_t* __restrict__ bstart, const int32_t* __restrict__ leaf_first,
+                             int chunk, int32_t* __restrict__ cbase) {
+  __shared__ int wt[32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int v = (bstart[t + 1] - bstart[t] + chunk - 1) / chunk + (leaf_first[t + 1] - leaf_first[t]);
+  int inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) wt[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const int sv = lane < PT_BUCKETS / 32 ? wt[lane] : 0;
+    int si = sv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(FULL, si, o);
+      if (lane >= o) si += u;
+    }
+    wt[lane] = si - sv;
+  }
+  __syncthreads();
+  cbase[t] = inc - v + wt[w];
 }
 
 // ---- incremental store update (delta ticks) -------------------------------
@@ -611,7 +714,8 @@ __global__ void k_leaf_subs(const int32_t* __restrict__ build_counts,
 // counts (0 past the last leaf)
 __global__ void k_leaf_bucket(const int32_t* __restrict__ pre, const int32_t* __restrict__ sub_base,
                               const int32_t* __restrict__ scalars, int64_t ncap,
-                              uint16_t* __restrict__ leaf_bucket, int32_t* __restrict__ bkey) {
+                              uint16_t* __restrict__ leaf_bucket, int32_t* __restrict__ bkey,
+                              int32_t* __restrict__ leaf_first) {
   const int64_t nl = scalars[1], n_sub = scalars[4];
   const int64_t nb = scalars[3] > 0 ? scalars[3] : 1;
   for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l <= nl && l < ncap + 1;
@@ -621,7 +725,10 @@ __global__ void k_leaf_bucket(const int32_t* __restrict__ pre, const int32_t* __
     const int bp = l == 0 ? -1 : (int)min((int64_t)pre[l - 1] * PT_BUCKETS / nb, (int64_t)PT_BUCKETS - 1);
     if (l < nl) leaf_bucket[l] = (uint16_t)b;
     const int32_t k0 = l < nl ? sub_base[l] : (int32_t)n_sub;
-    for (int bb = bp + 1; bb <= b; bb++) bkey[bb] = k0;  // buckets this leaf opens
+    for (int bb = bp + 1; bb <= b; bb++) {  // buckets this leaf opens
+      bkey[bb] = k0;
+      leaf_first[bb] = (int32_t)l;
+    }
   }
 }
 
@@ -775,6 +882,7 @@ int index_alloc(DevIndex& ix, int l_max, int th_quad) {
   MKNN_CUDA_OK(cudaMalloc(&ix.cell_info, sizeof(unsigned long long) * ncap));
   MKNN_CUDA_OK(cudaMalloc(&ix.bload, sizeof(uint32_t) * PT_BUCKETS));
   MKNN_CUDA_OK(cudaMalloc(&ix.bkey, sizeof(int32_t) * (PT_BUCKETS + 1)));
+  MKNN_CUDA_OK(cudaMalloc(&ix.leaf_first, sizeof(int32_t) * (PT_BUCKETS + 1)));
   MKNN_CUDA_OK(cudaMalloc(&ix.leaf_bucket, sizeof(uint16_t) * ncap));
   return 0;
 }
@@ -795,6 +903,7 @@ void index_free(DevIndex& ix) {
   cudaFree(ix.cell_info);
   cudaFree(ix.bload);
   cudaFree(ix.bkey);
+  cudaFree(ix.leaf_first);
   cudaFree(ix.leaf_bucket);
   ix = DevIndex{};
 }
@@ -852,7 +961,8 @@ int index_build(DevIndex& ix, const Region& r, const double* x, const double* y,
   rc = exclusive_scan_i32(lc, pre, ncap, scratch, s);
   if (rc) return rc;
   MKNN_LAUNCH k_leaf_bucket<<<blocks_for(ncap + 1), TPB, 0, s>>>(pre, ix.leaf_sub_base, ix.scalars, ncap,
-                                                                ix.leaf_bucket, ix.bkey);
+                                                                ix.leaf_bucket, ix.bkey,
+                                                                ix.leaf_first);
   MKNN_CUDA_OK(cudaMemsetAsync(ix.bload, 0, sizeof(uint32_t) * PT_BUCKETS, s));
   MKNN_LAUNCH k_bucket_load<<<blocks_for(ncap), TPB, 0, s>>>(ix.build_counts, ix.leaf_bucket,
                                                              ix.scalars, ncap, ix.bload);
@@ -882,8 +992,9 @@ int store_reserve(DevStore& st, int64_t n_sub, int64_t n_leaves, int64_t n) {
   if (!st.cursor) {
     MKNN_CUDA_OK(cudaMalloc(&st.cursor, sizeof(int32_t) * (PT_BUCKETS + 1)));
     MKNN_CUDA_OK(cudaMalloc(&st.bstart, sizeof(int32_t) * (PT_BUCKETS + 1)));
+    MKNN_CUDA_OK(cudaMalloc(&st.cbase, sizeof(int32_t) * (PT_BUCKETS + 1)));
   }
-  const int64_t nbox = n / (MAX_CHUNK / 2) + n_leaves + 1;
+  const int64_t nbox = n / (MAX_CHUNK / 2) + n_leaves + PT_BUCKETS + 1;  // + per-bucket slot rounding
   if (nbox > st.cap_box) {
     cudaFree(st.box);
     cudaFree(st.crange);
@@ -945,22 +1056,26 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
       MKNN_LAUNCH k_partition<<<(unsigned)((n + PT_TILE - 1) / PT_TILE), PT_THREADS, 0, s>>>(
           ids, x, y, st.key, n, bshift, st.cursor, st.rec, st.bkt);
     MKNN_CUDA_OK(cudaGetLastError());
-    const size_t smem = sizeof(int32_t) * BS_MAX_KEYS;
+    const size_t smem = sizeof(int32_t) * (3 * BS_MAX_KEYS + 1);
     static unsigned long long configured = 0;  // bit d: the attribute is set on device d
     int dev = 0;
     MKNN_CUDA_OK(cudaGetDevice(&dev));
     const unsigned long long bit = 1ull << (dev & 63);
     if (!(__atomic_load_n(&configured, __ATOMIC_ACQUIRE) & bit)) {
       MKNN_CUDA_OK(cudaFuncSetAttribute(k_bucket_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)(sizeof(int32_t) << 14)));
+                                        (int)smem));
       __atomic_fetch_or(&configured, bit, __ATOMIC_ACQ_REL);
     }
     int sms = 148;
     MKNN_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    MKNN_LAUNCH k_chunk_base<<<1, PT_BUCKETS, 0, s>>>(st.bstart, ix.leaf_first, st.chunk, st.cbase);
+    BucketLeaves bl{ix.leaf_first, ix.leaf_sub_base, st.cbase, st.cell_start, st.chunk_start,
+                    st.box, st.chunk, n_leaves};
     MKNN_LAUNCH k_bucket_sort<<<(unsigned)sms, BS_THREADS, smem, s>>>(st.rec, st.bstart, ix.bkey,
-                                                                       n_sub, n, st.kstart, st.obj);
+                                                                       n_sub, n, st.kstart, st.obj, bl);
     MKNN_CUDA_OK(cudaGetLastError());
-    return store_finish(st, ix, n, n_leaves, scratch, s);
+    st.n_store = n;
+    return 0;
   }
   if (st.dirty) {
     MKNN_CUDA_OK(cudaMemsetAsync(st.cnt, 0, sizeof(int32_t) * st.cap_sub, s));

@@ -68,6 +68,7 @@ struct DevIndex {
   unsigned long long* cell_info = nullptr;  // per deepest cell: sub_base | shift | bits | leaf
   uint32_t* bload = nullptr;  // rebuild scratch: build load per partition bucket
   int32_t* bkey = nullptr;       // leaf-aligned partition buckets: bucket b = keys [bkey[b], bkey[b+1])
+  int32_t* leaf_first = nullptr;  // bucket b holds leaves [leaf_first[b], leaf_first[b+1])
   uint16_t* leaf_bucket = nullptr;  // bucket of every leaf
   int l_max = 0;
   int th_quad = 0;
@@ -132,7 +133,8 @@ struct DevStore {
   uint16_t* bkt = nullptr;        // partition bucket per input object (bucket-local sort)
   int64_t cap = 0;
   int32_t* cell_start = nullptr;  // 4^l_max + 2 (start[L] = n)
-  int32_t* chunk_start = nullptr; // 4^l_max + 2 (chunk ordinal of each leaf's first chunk)
+  int32_t* chunk_start = nullptr; // 4^l_max + 2 (chunk slot of each leaf's first chunk; a leaf's
+                                  // chunks are [chunk_start[l], + ceil(population / chunk)))
   int32_t* nch = nullptr;         // 4^l_max + 2 scratch (chunks per leaf)
   ChunkBox* box = nullptr;        // per chunk
   int2* crange = nullptr;         // per chunk: object range
@@ -156,6 +158,7 @@ struct DevStore {
   int chunk = 32;                 // objects per chunk (chunk_for_k)
   int32_t* cursor = nullptr;      // bucket counts / cursors of the partition pass
   int32_t* bstart = nullptr;      // bucket starts
+  int32_t* cbase = nullptr;       // bucket-local sort: first chunk slot of every bucket
   int64_t cap_sub = 0;
   bool dirty = true;              // cnt must be cleared before use
 };

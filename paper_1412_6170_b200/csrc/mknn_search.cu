@@ -378,7 +378,7 @@ __device__ __forceinline__ void visit_leaf(List<KPL>& L, int k, int leaf, double
                                            long long me, const SearchArgs& a, int lane, bool own,
                                            double cap = DINF) {
   const int ob = __ldg(&a.cell_start[leaf]), oe = __ldg(&a.cell_start[leaf + 1]);
-  const int c0 = __ldg(&a.chunk_start[leaf]), c1 = __ldg(&a.chunk_start[leaf + 1]);
+  const int c0 = __ldg(&a.chunk_start[leaf]), c1 = c0 + (oe - ob + chunk_for_k(32 * KPL) - 1) / chunk_for_k(32 * KPL);
   prof_add(a.prof, own ? PROF_OWN_CHUNKS_TOTAL : PROF_EXP_CHUNKS_TOTAL, c1 - c0, lane);
   if (!own) prof_add(a.prof, PROF_EXP_LEAF_VISITS, 1, lane);
   bool scanned = false, admitted = false;  // profiling only
@@ -745,7 +745,7 @@ __device__ __forceinline__ void visit_leaf_buf(List<KPL>& L, int k, int leaf, do
                                                long long* rowi, bool own) {
   constexpr int N = 32 * KPL;
   const int ob = __ldg(&a.cell_start[leaf]), oe = __ldg(&a.cell_start[leaf + 1]);
-  const int c0 = __ldg(&a.chunk_start[leaf]), c1 = __ldg(&a.chunk_start[leaf + 1]);
+  const int c0 = __ldg(&a.chunk_start[leaf]), c1 = c0 + (oe - ob + chunk_for_k(32 * KPL) - 1) / chunk_for_k(32 * KPL);
   const unsigned lt = (1u << lane) - 1u;
   prof_add(a.prof, own ? PROF_OWN_CHUNKS_TOTAL : PROF_EXP_CHUNKS_TOTAL, c1 - c0, lane);
   if (!own) prof_add(a.prof, PROF_EXP_LEAF_VISITS, 1, lane);
@@ -1483,7 +1483,7 @@ __device__ __forceinline__ void visit1(L1& L, int k, int leaf, double qx, double
                                        const SearchArgs& a, int lane, bool own, double cap = DINF,
                                        LeafSrc src = LeafSrc{0u, 0u}) {
   const int ob = __ldg(&a.cell_start[leaf]), oe = __ldg(&a.cell_start[leaf + 1]);
-  const int c0 = __ldg(&a.chunk_start[leaf]), c1 = __ldg(&a.chunk_start[leaf + 1]);
+  const int c0 = __ldg(&a.chunk_start[leaf]), c1 = c0 + (oe - ob + chunk_for_k(32) - 1) / chunk_for_k(32);
   prof_add(a.prof, own ? PROF_OWN_CHUNKS_TOTAL : PROF_EXP_CHUNKS_TOTAL, c1 - c0, lane);
   if (!own) prof_add(a.prof, PROF_EXP_LEAF_VISITS, 1, lane);
   double kd;
@@ -1774,7 +1774,7 @@ __global__ void __launch_bounds__(32 * OWN_WARPS, OWN_CTAS_PER_SM) k_own1(const 
           ob = __ldg(&a.cell_start[l]);
           nr = __ldg(&a.cell_start[l + 1]) - ob;
           c0 = __ldg(&a.chunk_start[l]);
-          nx = __ldg(&a.chunk_start[l + 1]) - c0;
+          nx = (nr + chunk_for_k(32) - 1) / chunk_for_k(32);
         }
         // inclusive prefix of the leaders' sizes
         int pr = nr, px = nx;
@@ -2009,7 +2009,11 @@ static int batch_for(const SearchArgs& a, int by_density) {
   }
   int b = by_density;
   while (b > 4 && (a.nq + b - 1) / b < 2 * (int64_t)slots) b >>= 1;
-  return b;
+  static const int force = [] {  // MKNN_BATCH=4/8/16/32: A/B override
+    const char* e = getenv("MKNN_BATCH");
+    return e ? atoi(e) : 0;
+  }();
+  return force ? force : b;
 }
 
 int search_launch(const SearchArgs& a, cudaStream_t s) {
