@@ -231,6 +231,7 @@ struct mknn_engine {
   int64_t h_n_leaves = 0, h_overfull = 0, h_n_build = 0, h_n_sub = 0;
   int64_t h_bucket_load = 0;  // largest partition-bucket build load, 1/16 of the mean
   int64_t h_bucket_keys = 0;  // largest partition-bucket key count
+  bool two_pass_next = false;  // the last one-pass partition overflowed: redo in two passes
   DevStore st;
   DevQueries dq;
 
@@ -370,8 +371,9 @@ int alloc_store(mknn_engine* h, int64_t n) {
     }
     h->st.cap = 0;
     h->st.valid = false;
-    MKNN_CUDA_OK(cudaMalloc(&h->st.obj, sizeof(StoreRec) * nc));
-    MKNN_CUDA_OK(cudaMalloc(&h->st.rec, sizeof(StoreRec) * nc));
+    // obj and rec swap roles on incremental ticks: both hold a staging array
+    MKNN_CUDA_OK(cudaMalloc(&h->st.obj, sizeof(StoreRec) * staging_records(nc)));
+    MKNN_CUDA_OK(cudaMalloc(&h->st.rec, sizeof(StoreRec) * staging_records(nc)));
     MKNN_CUDA_OK(cudaMalloc(&h->st.key, sizeof(uint32_t) * nc));
     MKNN_CUDA_OK(cudaMalloc(&h->st.rmflag, sizeof(int32_t) * (nc + 1)));
     MKNN_CUDA_OK(cudaMalloc(&h->st.rm_before, sizeof(int32_t) * (nc + 2)));
@@ -478,7 +480,8 @@ int graph_key(mknn_engine* h, int64_t n, const long long* ids, const double* x, 
           (uintptr_t)o.offsets, (uintptr_t)o.nids, (uintptr_t)o.dist,
           (uintptr_t)h->scratch.p, (uintptr_t)h->pin, (uintptr_t)h->dq.bm_cap,
           (uintptr_t)h->st.cap_sub, (uintptr_t)h->st.cap_box, (uintptr_t)(h->n_spec >= 0),
-          (uintptr_t)h->h_bucket_load, (uintptr_t)h->h_bucket_keys};
+          (uintptr_t)h->h_bucket_load, (uintptr_t)h->h_bucket_keys, (uintptr_t)h->two_pass_next,
+          (uintptr_t)h->st.bcnt_valid};
   for (void* b : engine_buffers(h)) key->push_back((uintptr_t)b);
   *ok = true;
   return 0;
@@ -580,6 +583,7 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
       MKNN_CUDA_OK(cudaEventRecordWithFlags(h->ev[0], s, ev_flags));
       if (rebuild) {
         if ((rc = index_build(h->ix, h->r, x, y, n, h->scratch.p, s))) return h->set_err(rc);
+        h->st.bcnt_valid = false;  // new buckets: the next partition counts them exactly
         h->have_index = true;
         m.rebuild_flag = 1;
         if ((rc = refresh_index_info(h))) return h->set_err(rc);  // leaf count sizes the store tables
@@ -608,7 +612,8 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
       } else {
         if ((rc = store_index_objects(h->st, h->ix, h->r, ids, x, y, n, h->h_n_leaves, h->h_n_sub,
                                       h->h_bucket_load <= 4 * 16 && h->h_bucket_keys <= 16384,
-                                      h->counters + 3, h->scratch.p,
+                                      h->two_pass_next, h->counters + 3, h->counters + 4,
+                                      h->scratch.p,
                                       s)))
           return h->set_err(rc);
         MKNN_CUDA_OK(cudaMemcpyAsync(h->clamped_total, h->counters + 3, sizeof(unsigned long long),
@@ -751,6 +756,7 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
       if ((rc = stats_reduce(h->stats, nq, h->counters, h->hist, h->hist + h->hist_cap, h->hist_cap, s)))
         return h->set_err(rc);
       if ((rc = rows_compact(o.len, o.nids, o.dist, nq, k, o.offsets, h->out_nids, h->out_dist,
+                             h->dq.dup,
                              h->scratch.p, s)))
         return h->set_err(rc);
       MKNN_CUDA_OK(cudaEventRecordWithFlags(h->ev[5], s, ev_flags));
@@ -807,6 +813,16 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
     MKNN_CUDA_OK(cudaStreamSynchronize(h->copy_stream));
     h->rows_in_host = total == nq * (int64_t)k;  // short rows: the caller copies the CSR
   }
+  if (cnt[4]) {
+    // a bucket outgrew its planned staging region (one-pass partition):
+    // the store is incomplete -> redo the tick with the two-pass partition
+    *retry = true;
+    h->two_pass_next = true;
+    h->retry_rebuild = rebuild;
+    h->st.valid = false;  // the store is incomplete: no incremental redo on top of it
+    return 0;
+  }
+  h->two_pass_next = false;
   if (h->n_spec >= 0 && pb.nsnap != h->n_spec) {
     // the updates since the last confirmed size appended ids: the tick ran
     // on a short snapshot -> core_tick syncs the size and redoes it

@@ -31,7 +31,7 @@ constexpr int TPB = 256;
 constexpr int PT_THREADS = 512;
 constexpr int PT_ITEMS = 4;
 constexpr int PT_TILE = PT_THREADS * PT_ITEMS;
-constexpr int PT_BUCKETS = 1024;
+constexpr int PT_BUCKETS = 1024;  // staging_records() assumes 1024 x 256 records of region slack
 
 inline unsigned blocks_for(int64_t n, int per = TPB) {
   int64_t b = (n + per - 1) / per;
@@ -163,6 +163,10 @@ __device__ __forceinline__ void point_key(double xi, double yi, const Region& r,
   const int shift = (int)((e >> 32) & 63u), sb = (int)((e >> 38) & 15u);
   leaf = (uint32_t)(e >> 42);
   key = (uint32_t)e + ((f >> shift) & ((1u << sb) - 1u));
+}
+
+__device__ __forceinline__ bool outside(double x, double y, const Region& r) {
+  return (x < r.x_lo) | (x > r.x_hi) | (y < r.y_lo) | (y > r.y_hi);  // geometry.py:215-220
 }
 
 __global__ void k_point_keys(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
@@ -399,8 +403,9 @@ struct BucketLeaves {  // the leaf side of k_bucket_sort (store_finish's passes,
 // buckets in order so the second sweep finds its bucket in L2.
 __global__ void __launch_bounds__(BS_THREADS, 1) k_bucket_sort(
     const StoreRec* __restrict__ rec, const int32_t* __restrict__ bstart,
-    const int32_t* __restrict__ bkey, int64_t n_sub, int64_t n, int32_t* __restrict__ kstart,
-    StoreRec* __restrict__ obj, const BucketLeaves bl) {
+    const int32_t* __restrict__ sstart, const int32_t* __restrict__ bkey, int64_t n_sub, int64_t n,
+    int32_t* __restrict__ kstart, StoreRec* __restrict__ obj, const BucketLeaves bl) {
+  // bucket b's records: staging [sstart[b], + its count), store [bstart[b], bstart[b + 1])
   extern __shared__ int32_t sm[];
   int32_t* hist = sm;                   // BS_MAX_KEYS: key counts, then starts, then ends
   int32_t* lpre = sm + BS_MAX_KEYS;     // BS_MAX_KEYS + 1: chunks per leaf, then their prefix
@@ -415,15 +420,16 @@ __global__ void __launch_bounds__(BS_THREADS, 1) k_bucket_sort(
     const int kb = bkey[b];
     const int nk = bkey[b + 1] - kb;  // <= BS_MAX_KEYS (checked at the rebuild)
     const int bs = bstart[b], be = bstart[b + 1];
+    const StoreRec* __restrict__ src = rec + (sstart[b] - bs);  // src[i] for i in [bs, be)
     for (int j = t; j < nk; j += BS_THREADS) hist[j] = 0;
     __syncthreads();
-    for (int i = bs + t; i < be; i += BS_THREADS) atomicAdd(&hist[(int)__ldg(&rec[i].key) - kb], 1);
+    for (int i = bs + t; i < be; i += BS_THREADS) atomicAdd(&hist[(int)__ldg(&src[i].key) - kb], 1);
     __syncthreads();
     block_exclusive_scan(hist, nk, bs, wsum);
     for (int j = t; j < nk; j += BS_THREADS) kstart[kb + j] = hist[j];
     __syncthreads();
     for (int i = bs + t; i < be; i += BS_THREADS) {
-      const StoreRec r = ld_rec(&rec[i]);
+      const StoreRec r = ld_rec(&src[i]);
       st_rec(&obj[atomicAdd(&hist[(int)r.key - kb], 1)], r);
     }
     __syncthreads();
@@ -464,6 +470,146 @@ __global__ void __launch_bounds__(BS_THREADS, 1) k_bucket_sort(
     }
     __syncthreads();
   }
+}
+
+// One-pass partition (steady state): the staging regions of the buckets
+// are planned from the previous tick's bucket counts (or, after a rebuild,
+// the build loads) with 1/8 + 256 records of slack, so the key pass and the
+// partition are one kernel -- positions are read once.  A bucket that
+// outgrows its region raises *overflow (records beyond it are dropped) and
+// the tick is redone with the two-pass partition (exact counts).
+__global__ void k_cap_plan(const uint32_t* __restrict__ prev, int32_t* __restrict__ sstart,
+                           int32_t* __restrict__ cursor) {
+  __shared__ int wt[32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int c = (int)prev[t];
+  const int v = c + c / 8 + 256;
+  int inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) wt[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const int sv = lane < PT_BUCKETS / 32 ? wt[lane] : 0;
+    int si = sv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(FULL, si, o);
+      if (lane >= o) si += u;
+    }
+    wt[lane] = si - sv;
+  }
+  __syncthreads();
+  const int ex = inc - v + wt[w];
+  sstart[t] = ex;
+  cursor[t] = ex;
+  if (t == PT_BUCKETS - 1) sstart[PT_BUCKETS] = ex + v;
+}
+
+// the key pass (k_point_keys) and the partition (k_partition) in one: a
+// tile keys its objects, ranks them per bucket in shared memory and
+// reserves one run per bucket in the planned regions
+__global__ void __launch_bounds__(PT_THREADS) k_partition_keys(
+    const long long* __restrict__ ids, const double* __restrict__ x, const double* __restrict__ y,
+    int64_t n, Region r, const int32_t* __restrict__ scalars,
+    const unsigned long long* __restrict__ info, const uint16_t* __restrict__ leaf_bucket,
+    const int32_t* __restrict__ sstart, int32_t* __restrict__ cursor, StoreRec* __restrict__ out,
+    unsigned long long* clamped, unsigned long long* overflow) {
+  __shared__ int hist[PT_BUCKETS], gbase[PT_BUCKETS];
+  const int t = threadIdx.x;
+  const int64_t base = (int64_t)blockIdx.x * PT_TILE;
+  const int tile_n = (n - base) < PT_TILE ? (int)(n - base) : PT_TILE;
+  const int l_deep = scalars[0];
+  for (int i = t; i < PT_BUCKETS; i += PT_THREADS) hist[i] = 0;
+  StoreRec rc[PT_ITEMS];
+  int bk[PT_ITEMS];
+  unsigned outside_n = 0;
+#pragma unroll
+  for (int j = 0; j < PT_ITEMS; j++) {
+    const int li = t + j * PT_THREADS;
+    if (li < tile_n) {
+      const int64_t i = base + li;
+      rc[j].x = x[i];
+      rc[j].y = y[i];
+      rc[j].id = ids[i];
+      rc[j].pad = (uint32_t)i;  // input index (the snapshot slot on the delta path)
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < PT_ITEMS; j++) {
+    if (t + j * PT_THREADS < tile_n) {
+      // geometry.py:215-220 count_outside
+      outside_n += outside(rc[j].x, rc[j].y, r);
+      uint32_t leaf, key;
+      point_key(rc[j].x, rc[j].y, r, l_deep, info, leaf, key);
+      rc[j].key = key;
+      bk[j] = __ldg(&leaf_bucket[leaf]);
+    }
+  }
+  __syncthreads();
+  int rank[PT_ITEMS];
+#pragma unroll
+  for (int j = 0; j < PT_ITEMS; j++)
+    if (t + j * PT_THREADS < tile_n) rank[j] = atomicAdd(&hist[bk[j]], 1);
+  __syncthreads();
+  bool over = false;
+  for (int i = t; i < PT_BUCKETS; i += PT_THREADS)
+    if (hist[i]) {
+      gbase[i] = atomicAdd(&cursor[i], hist[i]);
+      over |= gbase[i] + hist[i] > sstart[i + 1];
+    }
+  if (over) atomicOr(overflow, 1ull);
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < PT_ITEMS; j++)
+    if (t + j * PT_THREADS < tile_n) {
+      const int pos = gbase[bk[j]] + rank[j];
+      if (pos < sstart[bk[j] + 1]) st_rec(&out[pos], rc[j]);
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) outside_n += __shfl_xor_sync(FULL, outside_n, o);
+  if ((t & 31) == 0 && outside_n) atomicAdd(clamped, (unsigned long long)outside_n);
+}
+
+// after the one-pass partition: each bucket's count (clipped to its
+// region), kept for the next tick's plan, and the store layout (bstart)
+__global__ void k_bucket_counts(const int32_t* __restrict__ sstart, const int32_t* __restrict__ cursor,
+                                uint32_t* __restrict__ counts, int32_t* __restrict__ bstart) {
+  __shared__ int wt[32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int v = min(cursor[t], sstart[t + 1]) - sstart[t];
+  counts[t] = (uint32_t)v;
+  int inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) wt[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const int sv = lane < PT_BUCKETS / 32 ? wt[lane] : 0;
+    int si = sv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(FULL, si, o);
+      if (lane >= o) si += u;
+    }
+    wt[lane] = si - sv;
+  }
+  __syncthreads();
+  const int ex = inc - v + wt[w];
+  bstart[t] = ex;
+  if (t == PT_BUCKETS - 1) bstart[PT_BUCKETS] = ex + v;
+}
+
+// two-pass partition: the exact bucket counts (k_point_keys' histogram,
+// then scanned in place into cursor) for the next tick's plan
+__global__ void k_save_counts(const int32_t* __restrict__ bstart, uint32_t* __restrict__ counts) {
+  counts[threadIdx.x] = (uint32_t)(bstart[threadIdx.x + 1] - bstart[threadIdx.x]);
 }
 
 // chunk slot bases of the buckets: an upper bound of each bucket's chunks
@@ -510,9 +656,6 @@ __global__ void k_key_counts(const int32_t* __restrict__ kstart, int64_t n_sub,
     cnt[i] = kstart[i + 1] - kstart[i];
 }
 
-__device__ __forceinline__ bool outside(double x, double y, const Region& r) {
-  return (x < r.x_lo) | (x > r.x_hi) | (y < r.y_lo) | (y > r.y_hi);  // geometry.py:215-220
-}
 
 // moved slot j: remove its old record (if it had one: found in its old key
 // group, a handful of records, by the slot the record carries), key its new
@@ -993,6 +1136,8 @@ int store_reserve(DevStore& st, int64_t n_sub, int64_t n_leaves, int64_t n) {
     MKNN_CUDA_OK(cudaMalloc(&st.cursor, sizeof(int32_t) * (PT_BUCKETS + 1)));
     MKNN_CUDA_OK(cudaMalloc(&st.bstart, sizeof(int32_t) * (PT_BUCKETS + 1)));
     MKNN_CUDA_OK(cudaMalloc(&st.cbase, sizeof(int32_t) * (PT_BUCKETS + 1)));
+    MKNN_CUDA_OK(cudaMalloc(&st.sstart, sizeof(int32_t) * (PT_BUCKETS + 1)));
+    MKNN_CUDA_OK(cudaMalloc(&st.bcnt, sizeof(uint32_t) * PT_BUCKETS));
   }
   const int64_t nbox = n / (MAX_CHUNK / 2) + n_leaves + PT_BUCKETS + 1;  // + per-bucket slot rounding
   if (nbox > st.cap_box) {
@@ -1032,8 +1177,8 @@ static int store_finish(DevStore& st, const DevIndex& ix, int64_t n, int64_t n_l
 
 int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const long long* ids,
                         const double* x, const double* y, int64_t n, int64_t n_leaves,
-                        int64_t n_sub, bool balanced, unsigned long long* dev_clamped,
-                        void* scratch, cudaStream_t s) {
+                        int64_t n_sub, bool balanced, bool two_pass, unsigned long long* dev_clamped,
+                        unsigned long long* dev_overflow, void* scratch, cudaStream_t s) {
   // MKNN_BSORT=0: the global-atomic counting sort (per-key counts in the
   // key pass, a scan over all sub-cells, an atomic final scatter) for A/B
   static const bool bsort = [] {
@@ -1044,17 +1189,32 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
   while ((std::max<int64_t>(n_sub, 1) - 1) >> bshift >= PT_BUCKETS) bshift++;
   // <= 2^24 sub-cells: a 64 KB histogram; buckets of <= 32K records (1 MB)
   // so the second sweep still finds them in L2 (100M objects: 6.20 -> 6.32 ms)
-  if (bsort && balanced && n <= (int64_t)PT_BUCKETS * 32768) {
-    MKNN_CUDA_OK(cudaMemsetAsync(st.cursor, 0, sizeof(int32_t) * PT_BUCKETS, s));
-    if (n > 0)
+  if (bsort && balanced && n <= (int64_t)PT_BUCKETS * 32768 && n > 0) {
+    // MKNN_ONEPASS=0: always the two-pass partition (A/B)
+    static const bool onepass = [] {
+      const char* e = getenv("MKNN_ONEPASS");
+      return !(e && e[0] == '0');
+    }();
+    const int32_t* sstart = st.bstart;  // two-pass: staging and store share the layout
+    if (onepass && st.bcnt_valid && !two_pass) {
+      MKNN_LAUNCH k_cap_plan<<<1, PT_BUCKETS, 0, s>>>(st.bcnt, st.sstart, st.cursor);
+      MKNN_LAUNCH k_partition_keys<<<(unsigned)((n + PT_TILE - 1) / PT_TILE), PT_THREADS, 0, s>>>(
+          ids, x, y, n, r, ix.scalars, ix.cell_info, ix.leaf_bucket, st.sstart, st.cursor, st.rec,
+          dev_clamped, dev_overflow);
+      MKNN_LAUNCH k_bucket_counts<<<1, PT_BUCKETS, 0, s>>>(st.sstart, st.cursor, st.bcnt, st.bstart);
+      sstart = st.sstart;
+    } else {
+      MKNN_CUDA_OK(cudaMemsetAsync(st.cursor, 0, sizeof(int32_t) * PT_BUCKETS, s));
       MKNN_LAUNCH k_point_keys<<<grid_stride_blocks(n), TPB, 0, s>>>(
           x, y, n, r, ix.scalars, ix.cell_info, nullptr, st.key, nullptr, dev_clamped, bshift,
           st.cursor, ix.leaf_bucket, st.bkt);
-    MKNN_CUDA_OK(cudaGetLastError());
-    MKNN_LAUNCH k_bucket_scan<<<1, PT_BUCKETS, 0, s>>>(st.cursor, st.bstart, st.cursor);
-    if (n > 0)
+      MKNN_CUDA_OK(cudaGetLastError());
+      MKNN_LAUNCH k_bucket_scan<<<1, PT_BUCKETS, 0, s>>>(st.cursor, st.bstart, st.cursor);
       MKNN_LAUNCH k_partition<<<(unsigned)((n + PT_TILE - 1) / PT_TILE), PT_THREADS, 0, s>>>(
           ids, x, y, st.key, n, bshift, st.cursor, st.rec, st.bkt);
+      MKNN_LAUNCH k_save_counts<<<1, PT_BUCKETS, 0, s>>>(st.bstart, st.bcnt);
+      st.bcnt_valid = true;
+    }
     MKNN_CUDA_OK(cudaGetLastError());
     const size_t smem = sizeof(int32_t) * (3 * BS_MAX_KEYS + 1);
     static unsigned long long configured = 0;  // bit d: the attribute is set on device d
@@ -1071,7 +1231,7 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
     MKNN_LAUNCH k_chunk_base<<<1, PT_BUCKETS, 0, s>>>(st.bstart, ix.leaf_first, st.chunk, st.cbase);
     BucketLeaves bl{ix.leaf_first, ix.leaf_sub_base, st.cbase, st.cell_start, st.chunk_start,
                     st.box, st.chunk, n_leaves};
-    MKNN_LAUNCH k_bucket_sort<<<(unsigned)sms, BS_THREADS, smem, s>>>(st.rec, st.bstart, ix.bkey,
+    MKNN_LAUNCH k_bucket_sort<<<(unsigned)sms, BS_THREADS, smem, s>>>(st.rec, st.bstart, sstart, ix.bkey,
                                                                        n_sub, n, st.kstart, st.obj, bl);
     MKNN_CUDA_OK(cudaGetLastError());
     st.n_store = n;

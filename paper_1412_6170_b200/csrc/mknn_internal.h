@@ -159,9 +159,17 @@ struct DevStore {
   int32_t* cursor = nullptr;      // bucket counts / cursors of the partition pass
   int32_t* bstart = nullptr;      // bucket starts
   int32_t* cbase = nullptr;       // bucket-local sort: first chunk slot of every bucket
+  int32_t* sstart = nullptr;      // one-pass partition: staging region start of every bucket
+  uint32_t* bcnt = nullptr;       // bucket counts of the last bucket-sorted tick (plans the regions)
+  bool bcnt_valid = false;        // bcnt matches the current index's buckets
   int64_t cap_sub = 0;
   bool dirty = true;              // cnt must be cleared before use
 };
+
+// records of the store and of its staging array for a capacity of n objects:
+// the one-pass partition plans every bucket's region with 1/8 + 256 records
+// of slack over the last tick's count (1024 buckets)
+inline int64_t staging_records(int64_t n) { return n + n / 8 + 1024 * 256 + 1024; }
 
 // (re)size the sub-cell tables and chunk arrays for n objects
 int store_reserve(DevStore& st, int64_t n_sub, int64_t n_leaves, int64_t n);
@@ -173,10 +181,14 @@ int store_reserve(DevStore& st, int64_t n_sub, int64_t n_leaves, int64_t n);
 // balanced: the partition buckets' build loads are near the mean (DevIndex
 // scalars[5]), so the bucket-local sort is used; otherwise the global-atomic
 // counting sort
+// two_pass: the bucket-local sort keys and partitions in two passes (exact
+// bucket counts) instead of one pass over regions planned from the last
+// tick's counts; *dev_overflow != 0 after a one-pass tick whose bucket
+// outgrew its region (the caller redoes the tick with two_pass)
 int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const long long* ids,
                         const double* x, const double* y, int64_t n, int64_t n_leaves,
-                        int64_t n_sub, bool balanced, unsigned long long* dev_clamped,
-                        void* scratch, cudaStream_t s);
+                        int64_t n_sub, bool balanced, bool two_pass, unsigned long long* dev_clamped,
+                        unsigned long long* dev_overflow, void* scratch, cudaStream_t s);
 // Delta tick over the snapshot (sids/sx/sy, n_new slots): moved[0, m) are
 // the slots whose position changed (or were appended) since the store was
 // built from that snapshot.  dev_clamped_total: persistent count of objects
@@ -283,8 +295,10 @@ int stats_reduce(const QueryStats* st, int64_t nq, unsigned long long* dev_tot, 
 // padded rows (written by the search into the output itself) -> CSR in
 // place: offsets[nq + 1] (int64); t_nids / t_dist are [nq * k] scratch
 // touched only when some row is short
+// skip (device flag, may be null): non-zero when the tick will be redone
+// (its rows are not all written), so nothing is moved
 int rows_compact(const int32_t* len, long long* nids, double* dist, int64_t nq, int k,
-                 int64_t* offsets, long long* t_nids, double* t_dist, void* scratch,
-                 cudaStream_t s);
+                 int64_t* offsets, long long* t_nids, double* t_dist, const int32_t* skip,
+                 void* scratch, cudaStream_t s);
 
 }  // namespace mknn

@@ -1919,11 +1919,14 @@ __global__ void k_stats_reduce(const QueryStats* __restrict__ st, int64_t nq,
 // other than the issuer) == k, the common case).  Otherwise the rows are
 // moved to `tmp` and compacted back.  Both kernels read the CSR total on the
 // device and return at once when every row is full (no host round trip).
+// skip: the tick is redone (issuer ids repeated or beyond the planned range:
+// some rows were never written, so the lengths are not trustworthy)
 __global__ void k_rows_stash(const int64_t* __restrict__ off, int64_t nq, int k,
                              const long long* __restrict__ nids, const double* __restrict__ dist,
-                             long long* __restrict__ t_nids, double* __restrict__ t_dist) {
+                             long long* __restrict__ t_nids, double* __restrict__ t_dist,
+                             const int32_t* __restrict__ skip) {
   const int64_t total = nq * (int64_t)k;
-  if (off[nq] == total) return;
+  if (off[nq] == total || (skip && *skip)) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     t_nids[i] = nids[i];
@@ -1934,9 +1937,9 @@ __global__ void k_rows_stash(const int64_t* __restrict__ off, int64_t nq, int k,
 __global__ void k_rows_compact(const int32_t* __restrict__ len, const long long* __restrict__ nids,
                                const double* __restrict__ dist, int64_t nq, int k,
                                const int64_t* __restrict__ off, long long* __restrict__ c_nids,
-                               double* __restrict__ c_dist) {
+                               double* __restrict__ c_dist, const int32_t* __restrict__ skip) {
   const int64_t total = nq * (int64_t)k;
-  if (off[nq] == total) return;
+  if (off[nq] == total || (skip && *skip)) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / k;
@@ -2088,16 +2091,16 @@ int stats_reduce(const QueryStats* st, int64_t nq, unsigned long long* dev_tot, 
 }
 
 int rows_compact(const int32_t* len, long long* nids, double* dist, int64_t nq, int k,
-                 int64_t* offsets, long long* t_nids, double* t_dist, void* scratch,
+                 int64_t* offsets, long long* t_nids, double* t_dist, const int32_t* skip, void* scratch,
                  cudaStream_t s) {
   int rc = exclusive_scan_i32_to_i64(len, offsets, nq, scratch, s);
   if (rc) return rc;
   if (nq == 0) return 0;
   const int64_t total = nq * (int64_t)k;
   const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
-  MKNN_LAUNCH k_rows_stash<<<(unsigned)blocks, 256, 0, s>>>(offsets, nq, k, nids, dist, t_nids, t_dist);
+  MKNN_LAUNCH k_rows_stash<<<(unsigned)blocks, 256, 0, s>>>(offsets, nq, k, nids, dist, t_nids, t_dist, skip);
   MKNN_LAUNCH k_rows_compact<<<(unsigned)blocks, 256, 0, s>>>(len, t_nids, t_dist, nq, k, offsets, nids,
-                                                             dist);
+                                                             dist, skip);
   MKNN_CUDA_OK(cudaGetLastError());
   return 0;
 }

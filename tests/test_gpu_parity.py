@@ -257,6 +257,31 @@ def test_graph_replay_equals_direct(k):
         assert rep >= 3, (cap, rep)
 
 
+def test_onepass_partition_overflow_redo():
+    """Steady-state ticks partition the store in one pass over bucket regions
+    planned from the previous tick's counts; when the objects pile into a few
+    leaves without a rebuild, a bucket outgrows its region and the tick is
+    redone with the two-pass partition -- every tick still equals the oracle."""
+    rng = np.random.default_rng(21)
+    n, k = 60_000, 16
+    snap = synth.place(n, "uniform", seed=8)
+    x, y = snap.x.copy(), snap.y.copy()
+    with Engine(EngineConfig(k=k, region=synth.REGION, rebuild_window=50)) as eng:
+        for t in range(5):
+            if t == 2:  # 80 % of the objects jump into one small square
+                sel = rng.random(n) < 0.8
+                x[sel] = rng.uniform(1000.0, 1300.0, sel.sum())
+                y[sel] = rng.uniform(2000.0, 2300.0, sel.sum())
+            elif t > 0:
+                x = np.clip(x + rng.normal(0, 5.0, n), 0, 22500)
+                y = np.clip(y + rng.normal(0, 5.0, n), 0, 22500)
+            qsel = rng.choice(n, 3000, replace=False)
+            qi, qx, qy = snap.ids[qsel], x[qsel], y[qsel]
+            res = eng.process_tick(snap.ids, x, y, qi, qx, qy)
+            assert eng.last_metrics.rebuild_flag == (1 if t == 0 else 0)
+            assert_same(res, orc.brute_force_knn(snap.ids, x, y, qi, qx, qy, k))
+
+
 def test_device_calls_follow_the_torch_stream():
     """Tensors produced on a side stream (async pinned copies, a sleep kernel
     ahead of them) feed update/query_device/tick_device on that stream: the
