@@ -204,6 +204,8 @@ class Engine:
         self._user_stream = False
         self._bound_stream = 0
         self._ramp = np.zeros(0, np.int64)  # 0..nq, reused for full-row CSR offsets
+        self._act_buf = None  # active-count readback buffer (_finish)
+        self._act_ptr = None
 
     # -- lifecycle (engine.py:570-585) --------------------------------------
     def _handle(self):
@@ -330,11 +332,17 @@ class Engine:
     def _finish(self, m: N.Metrics) -> TickMetrics:
         L = N.lib()
         act = []
+        if self._act_buf is None:
+            self._act_buf = np.empty(256, np.int64)
+            self._act_ptr = self._act_buf.ctypes.data_as(N._i64p)
         for d in (0, 1):
-            cnt = L.mknn_active_counts(self._h, d, None, 0)
-            buf = np.empty(max(cnt, 1), np.int64)
-            L.mknn_active_counts(self._h, d, buf.ctypes.data_as(N._i64p), cnt)
-            act.append([int(v) for v in buf[:cnt]])
+            # one call in the common case (<= 256 iterations per direction)
+            cnt = L.mknn_active_counts(self._h, d, self._act_ptr, len(self._act_buf))
+            if cnt > len(self._act_buf):
+                self._act_buf = np.empty(cnt, np.int64)
+                self._act_ptr = self._act_buf.ctypes.data_as(N._i64p)
+                L.mknn_active_counts(self._h, d, self._act_ptr, cnt)
+            act.append(self._act_buf[:cnt].tolist())
         tm = TickMetrics(
             tick=m.tick, n_objects=m.n_objects, n_queries=m.n_queries,
             iterations_left=m.iterations_left, iterations_right=m.iterations_right,
