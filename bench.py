@@ -257,6 +257,9 @@ def run_reference(args, wl):
         return 0
     snap, qi, qx, qy = make_inputs(wl)
     th = resolve_th_quad("auto", wl["k"])
+    # every host thread (torchrun sets OMP_NUM_THREADS=1 per process; rank 0
+    # alone runs this arm, so it may use the whole host)
+    orc.set_num_threads(os.cpu_count() or 1)
     index = orc.build_index(snap.x, snap.y, synth.REGION, th, 10)  # the first tick's rebuild
     for _ in range(args.warmup):  # warm-up: the re-index and a small query batch
         cpu_port_tick_seconds(snap, qi, qx, qy, wl["k"], synth.REGION, th, 1000, index=index)
