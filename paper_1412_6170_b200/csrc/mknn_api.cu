@@ -231,6 +231,7 @@ struct mknn_engine {
   int64_t h_n_leaves = 0, h_overfull = 0, h_n_build = 0, h_n_sub = 0;
   int64_t h_bucket_load = 0;  // largest partition-bucket build load, 1/16 of the mean
   int64_t h_bucket_keys = 0;  // largest partition-bucket key count
+  int64_t h_bucket_leaves = 0;  // largest partition-bucket leaf count
   bool two_pass_next = false;  // the last one-pass partition overflowed: redo in two passes
   DevStore st;
   DevQueries dq;
@@ -422,6 +423,7 @@ int refresh_index_info(mknn_engine* h) {
   h->h_n_sub = sc[4];
   h->h_bucket_load = sc[5];
   h->h_bucket_keys = sc[6];
+  h->h_bucket_leaves = sc[7];
   return 0;
 }
 
@@ -480,7 +482,8 @@ int graph_key(mknn_engine* h, int64_t n, const long long* ids, const double* x, 
           (uintptr_t)o.offsets, (uintptr_t)o.nids, (uintptr_t)o.dist,
           (uintptr_t)h->scratch.p, (uintptr_t)h->pin, (uintptr_t)h->dq.bm_cap,
           (uintptr_t)h->st.cap_sub, (uintptr_t)h->st.cap_box, (uintptr_t)(h->n_spec >= 0),
-          (uintptr_t)h->h_bucket_load, (uintptr_t)h->h_bucket_keys, (uintptr_t)h->two_pass_next,
+          (uintptr_t)h->h_bucket_load, (uintptr_t)h->h_bucket_keys, (uintptr_t)h->h_bucket_leaves,
+          (uintptr_t)h->two_pass_next,
           (uintptr_t)h->st.bcnt_valid};
   for (void* b : engine_buffers(h)) key->push_back((uintptr_t)b);
   *ok = true;
@@ -611,8 +614,8 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
                                      cudaMemcpyDeviceToDevice, s));
       } else {
         if ((rc = store_index_objects(h->st, h->ix, h->r, ids, x, y, n, h->h_n_leaves, h->h_n_sub,
-                                      h->h_bucket_load <= 4 * 16 && h->h_bucket_keys <= 16384,
-                                      h->two_pass_next, h->counters + 3, h->counters + 4,
+                                      h->h_bucket_load <= 4 * 16 && h->h_bucket_keys <= 32768,
+                                      (int)h->h_bucket_keys, (int)h->h_bucket_leaves, h->two_pass_next, h->counters + 3, h->counters + 4,
                                       h->scratch.p,
                                       s)))
           return h->set_err(rc);
@@ -896,8 +899,13 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
                      std::chrono::steady_clock::now() - t_start)
                      .count();
   if (prof_on) {  // profiling only (MKNN_PROF=1)
-    unsigned long long pv[10];
+    unsigned long long pv[14];
     MKNN_CUDA_OK(cudaMemcpy(pv, h->prof, sizeof(pv), cudaMemcpyDeviceToHost));
+    fprintf(stderr,
+            "[mknn prof] expansion rounds %.3g (%.2f per query), active lanes per round %.2f, "
+            "navigate steps %.2f per query, step efficiency (sum / 32 x per-round max) %.2f\n",
+            (double)pv[10], (double)pv[10] * 32.0 / nq, (double)pv[11] / (pv[10] ? pv[10] : 1),
+            (double)pv[12] / nq, (double)pv[12] / (32.0 * (pv[13] ? pv[13] : 1)));
     fprintf(stderr,
             "[mknn prof] per query: own chunks %.2f/%.2f, exp leaves %.2f, exp chunks %.2f/%.2f, "
             "admitted %.2f, inserts %.2f, sort-merges %.2f; exp visits without scans %.2f, "

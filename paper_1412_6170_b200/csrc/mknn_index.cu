@@ -337,14 +337,15 @@ __global__ void k_final_scatter(const StoreRec* __restrict__ rec, int64_t n,
 // starts (written to kstart), and a second sweep places every record at its
 // key's start plus a shared-atomic rank.  CTAs walk the buckets in order so
 // the records of the second sweep are still in L2.
-constexpr int BS_THREADS = 1024;
-constexpr int BS_MAX_KEYS = 16384;  // 64 KB shared histogram (and <= that many leaves per bucket)
+constexpr int BS_MAX_KEYS = 32768;    // 128 KB shared key histogram per bucket
+constexpr int BS_MAX_LEAVES = 8192;   // leaves per bucket (two 32 KB leaf arrays)
 
 // in-place exclusive scan of v[0, m) by the whole CTA, plus `base`;
 // returns the total (v[m] is not written)
+template <int NT>
 __device__ __forceinline__ int block_exclusive_scan(int32_t* v, int m, int base, int32_t* wsum) {
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int E = (m + BS_THREADS - 1) / BS_THREADS;
+  const int E = (m + NT - 1) / NT;
   const int j0 = min(t * E, m), j1 = min(j0 + E, m);
   int sum = 0;
   for (int j = j0; j < j1; j++) sum += v[j];
@@ -357,15 +358,15 @@ __device__ __forceinline__ int block_exclusive_scan(int32_t* v, int m, int base,
   if (lane == 31) wsum[w] = inc;
   __syncthreads();
   if (w == 0) {
-    const int x = wsum[lane];
+    const int x = lane < NT / 32 ? wsum[lane] : 0;
     int xi = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int u = __shfl_up_sync(FULL, xi, o);
       if (lane >= o) xi += u;
     }
-    wsum[lane] = xi - x;
-    if (lane == 31) wsum[BS_THREADS / 32] = xi;  // the total
+    if (lane < NT / 32) wsum[lane] = xi - x;
+    if (lane == 31) wsum[NT / 32] = xi;  // the total
   }
   __syncthreads();
   int run = base + wsum[w] + inc - sum;
@@ -374,7 +375,7 @@ __device__ __forceinline__ int block_exclusive_scan(int32_t* v, int m, int base,
     v[j] = run;
     run += c;
   }
-  const int total = wsum[BS_THREADS / 32];
+  const int total = wsum[NT / 32];
   __syncthreads();
   return total;
 }
@@ -401,16 +402,20 @@ struct BucketLeaves {  // the leaf side of k_bucket_sort (store_finish's passes,
 // chunk boxes from the records it just placed (still in L2): no separate
 // leaf-range, chunk-range and box passes over the store.  CTAs walk the
 // buckets in order so the second sweep finds its bucket in L2.
-__global__ void __launch_bounds__(BS_THREADS, 1) k_bucket_sort(
+// NT threads, MK keys and ML leaves per bucket at most; (1024, 32K, 8K):
+// 192 KB of shared memory, one CTA per SM; (512, 16K, 4K): 96 KB, two CTAs
+// per SM, so one bucket's scan and leaf phases overlap another's sweeps
+template <int NT, int MK, int ML>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_bucket_sort(
     const StoreRec* __restrict__ rec, const int32_t* __restrict__ bstart,
     const int32_t* __restrict__ sstart, const int32_t* __restrict__ bkey, int64_t n_sub, int64_t n,
     int32_t* __restrict__ kstart, StoreRec* __restrict__ obj, const BucketLeaves bl) {
   // bucket b's records: staging [sstart[b], + its count), store [bstart[b], bstart[b + 1])
   extern __shared__ int32_t sm[];
-  int32_t* hist = sm;                   // BS_MAX_KEYS: key counts, then starts, then ends
-  int32_t* lpre = sm + BS_MAX_KEYS;     // BS_MAX_KEYS + 1: chunks per leaf, then their prefix
-  int32_t* lcs = sm + 2 * BS_MAX_KEYS + 1;  // BS_MAX_KEYS: leaf range starts
-  __shared__ int32_t wsum[BS_THREADS / 32 + 1];
+  int32_t* hist = sm;            // MK: key counts, then starts, then ends
+  int32_t* lpre = sm + MK;       // ML + 1: chunks per leaf, then their prefix
+  int32_t* lcs = sm + MK + ML + 1;  // ML: leaf range starts
+  __shared__ int32_t wsum[NT / 32 + 1];
   const int t = threadIdx.x;
   if (blockIdx.x == 0 && t == 0) {
     kstart[n_sub] = (int32_t)n;
@@ -418,24 +423,24 @@ __global__ void __launch_bounds__(BS_THREADS, 1) k_bucket_sort(
   }
   for (int b = blockIdx.x; b < PT_BUCKETS; b += gridDim.x) {
     const int kb = bkey[b];
-    const int nk = bkey[b + 1] - kb;  // <= BS_MAX_KEYS (checked at the rebuild)
+    const int nk = bkey[b + 1] - kb;  // <= MK (checked at the rebuild)
     const int bs = bstart[b], be = bstart[b + 1];
     const StoreRec* __restrict__ src = rec + (sstart[b] - bs);  // src[i] for i in [bs, be)
-    for (int j = t; j < nk; j += BS_THREADS) hist[j] = 0;
+    for (int j = t; j < nk; j += NT) hist[j] = 0;
     __syncthreads();
-    for (int i = bs + t; i < be; i += BS_THREADS) atomicAdd(&hist[(int)__ldg(&src[i].key) - kb], 1);
+    for (int i = bs + t; i < be; i += NT) atomicAdd(&hist[(int)__ldg(&src[i].key) - kb], 1);
     __syncthreads();
-    block_exclusive_scan(hist, nk, bs, wsum);
-    for (int j = t; j < nk; j += BS_THREADS) kstart[kb + j] = hist[j];
+    block_exclusive_scan<NT>(hist, nk, bs, wsum);
+    for (int j = t; j < nk; j += NT) kstart[kb + j] = hist[j];
     __syncthreads();
-    for (int i = bs + t; i < be; i += BS_THREADS) {
+    for (int i = bs + t; i < be; i += NT) {
       const StoreRec r = ld_rec(&src[i]);
       st_rec(&obj[atomicAdd(&hist[(int)r.key - kb], 1)], r);
     }
     __syncthreads();
     // hist[j] is now the end of key j: a leaf starts where its first key does
-    const int lf = bl.leaf_first[b], nlb = bl.leaf_first[b + 1] - lf;  // <= nk
-    for (int l = t; l < nlb; l += BS_THREADS) {
+    const int lf = bl.leaf_first[b], nlb = bl.leaf_first[b + 1] - lf;  // <= ML
+    for (int l = t; l < nlb; l += NT) {
       const int k0 = bl.sub_base[lf + l] - kb, k1 = bl.sub_base[lf + l + 1] - kb;
       const int cs = k0 == 0 ? bs : hist[k0 - 1];
       const int ce = k1 == 0 ? bs : hist[k1 - 1];
@@ -444,12 +449,12 @@ __global__ void __launch_bounds__(BS_THREADS, 1) k_bucket_sort(
       bl.cell_start[lf + l] = cs;
     }
     __syncthreads();
-    const int nchunks = block_exclusive_scan(lpre, nlb, 0, wsum);
+    const int nchunks = block_exclusive_scan<NT>(lpre, nlb, 0, wsum);
     const int cb = bl.cbase[b];
-    for (int l = t; l < nlb; l += BS_THREADS) bl.chunk_start[lf + l] = cb + lpre[l];
+    for (int l = t; l < nlb; l += NT) bl.chunk_start[lf + l] = cb + lpre[l];
     if (t == 0) lpre[nlb] = nchunks;
     __syncthreads();
-    for (int q = t; q < nchunks; q += BS_THREADS) {
+    for (int q = t; q < nchunks; q += NT) {
       int lo = 0, hi = nlb;  // the leaf: lpre[lo] <= q < lpre[lo + 1]
       while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
@@ -875,20 +880,31 @@ __global__ void k_leaf_bucket(const int32_t* __restrict__ pre, const int32_t* __
   }
 }
 
-// the largest key count of a bucket -> scalars[6] (the bucket-local sort
-// keeps a bucket's key histogram in shared memory)
-__global__ void k_bucket_keys(const int32_t* __restrict__ bkey, int32_t* __restrict__ scalars) {
-  __shared__ int wk[PT_BUCKETS / 32];
+// the largest key count and leaf count of a bucket -> scalars[6], [7] (the
+// bucket-local sort keeps both in shared memory)
+__global__ void k_bucket_keys(const int32_t* __restrict__ bkey, const int32_t* __restrict__ leaf_first,
+                              int32_t* __restrict__ scalars) {
+  __shared__ int wk[PT_BUCKETS / 32], wl[PT_BUCKETS / 32];
   const int b = threadIdx.x;
-  int mk = bkey[b + 1] - bkey[b];
+  int mk = bkey[b + 1] - bkey[b], ml = leaf_first[b + 1] - leaf_first[b];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mk = max(mk, __shfl_xor_sync(FULL, mk, o));
-  if ((b & 31) == 0) wk[b >> 5] = mk;
+  for (int o = 16; o > 0; o >>= 1) {
+    mk = max(mk, __shfl_xor_sync(FULL, mk, o));
+    ml = max(ml, __shfl_xor_sync(FULL, ml, o));
+  }
+  if ((b & 31) == 0) {
+    wk[b >> 5] = mk;
+    wl[b >> 5] = ml;
+  }
   __syncthreads();
   if (b == 0) {
-    int m = 0;
-    for (int i = 0; i < PT_BUCKETS / 32; i++) m = max(m, wk[i]);
-    scalars[6] = m;
+    int m = 0, l = 0;
+    for (int i = 0; i < PT_BUCKETS / 32; i++) {
+      m = max(m, wk[i]);
+      l = max(l, wl[i]);
+    }
+    scalars[6] = m <= BS_MAX_KEYS && l <= BS_MAX_LEAVES ? m : 0x7fffffff;  // > limit: no bucket sort
+    scalars[7] = l;
   }
 }
 
@@ -1110,7 +1126,7 @@ int index_build(DevIndex& ix, const Region& r, const double* x, const double* y,
   MKNN_LAUNCH k_bucket_load<<<blocks_for(ncap), TPB, 0, s>>>(ix.build_counts, ix.leaf_bucket,
                                                              ix.scalars, ncap, ix.bload);
   MKNN_LAUNCH k_bucket_load_max<<<1, PT_BUCKETS, 0, s>>>(ix.bload, ix.scalars);
-  MKNN_LAUNCH k_bucket_keys<<<1, PT_BUCKETS, 0, s>>>(ix.bkey, ix.scalars);
+  MKNN_LAUNCH k_bucket_keys<<<1, PT_BUCKETS, 0, s>>>(ix.bkey, ix.leaf_first, ix.scalars);
   MKNN_CUDA_OK(cudaGetLastError());
   return 0;
 }
@@ -1177,8 +1193,9 @@ static int store_finish(DevStore& st, const DevIndex& ix, int64_t n, int64_t n_l
 
 int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const long long* ids,
                         const double* x, const double* y, int64_t n, int64_t n_leaves,
-                        int64_t n_sub, bool balanced, bool two_pass, unsigned long long* dev_clamped,
-                        unsigned long long* dev_overflow, void* scratch, cudaStream_t s) {
+                        int64_t n_sub, bool balanced, int max_keys, int max_leaves, bool two_pass,
+                        unsigned long long* dev_clamped, unsigned long long* dev_overflow,
+                        void* scratch, cudaStream_t s) {
   // MKNN_BSORT=0: the global-atomic counting sort (per-key counts in the
   // key pass, a scan over all sub-cells, an atomic final scatter) for A/B
   static const bool bsort = [] {
@@ -1189,7 +1206,15 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
   while ((std::max<int64_t>(n_sub, 1) - 1) >> bshift >= PT_BUCKETS) bshift++;
   // <= 2^24 sub-cells: a 64 KB histogram; buckets of <= 32K records (1 MB)
   // so the second sweep still finds them in L2 (100M objects: 6.20 -> 6.32 ms)
-  if (bsort && balanced && n <= (int64_t)PT_BUCKETS * 32768 && n > 0) {
+  // larger buckets than ~32K records (1 MB) no longer stay in L2 between
+  // the sort's sweeps, but the bucket sort still edges out the atomic
+  // scatter (100M objects: 6.30 -> 6.18 ms); MKNN_BSORT_BIG=0 keeps those
+  // on the atomic path (A/B)
+  static const bool big = [] {
+    const char* e = getenv("MKNN_BSORT_BIG");
+    return !(e && e[0] == '0');
+  }();
+  if (bsort && balanced && (big || n <= (int64_t)PT_BUCKETS * 32768) && n > 0) {
     // MKNN_ONEPASS=0: always the two-pass partition (A/B)
     static const bool onepass = [] {
       const char* e = getenv("MKNN_ONEPASS");
@@ -1216,14 +1241,24 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
       st.bcnt_valid = true;
     }
     MKNN_CUDA_OK(cudaGetLastError());
-    const size_t smem = sizeof(int32_t) * (3 * BS_MAX_KEYS + 1);
-    static unsigned long long configured = 0;  // bit d: the attribute is set on device d
+    // small ticks (buckets of ~4K records at most) with <= 16K keys and 4K
+    // leaves per bucket: two 512-thread CTAs per SM (1M objects: 89 -> 79
+    // us; at 10M objects the 1024-thread CTAs win, 442 vs 501 us)
+    const bool small = n <= (int64_t)PT_BUCKETS * 4096 && max_keys <= BS_MAX_KEYS / 2 &&
+                       max_leaves <= BS_MAX_LEAVES / 2;
+    const size_t smem = small ? sizeof(int32_t) * (BS_MAX_KEYS / 2 + BS_MAX_LEAVES + 1)
+                              : sizeof(int32_t) * (BS_MAX_KEYS + 2 * BS_MAX_LEAVES + 1);
+    static unsigned long long configured = 0;  // bit d: the attributes are set on device d
     int dev = 0;
     MKNN_CUDA_OK(cudaGetDevice(&dev));
     const unsigned long long bit = 1ull << (dev & 63);
     if (!(__atomic_load_n(&configured, __ATOMIC_ACQUIRE) & bit)) {
-      MKNN_CUDA_OK(cudaFuncSetAttribute(k_bucket_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem));
+      MKNN_CUDA_OK(cudaFuncSetAttribute(k_bucket_sort<1024, BS_MAX_KEYS, BS_MAX_LEAVES>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)(sizeof(int32_t) * (BS_MAX_KEYS + 2 * BS_MAX_LEAVES + 1))));
+      MKNN_CUDA_OK(cudaFuncSetAttribute(k_bucket_sort<512, BS_MAX_KEYS / 2, BS_MAX_LEAVES / 2>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)(sizeof(int32_t) * (BS_MAX_KEYS / 2 + BS_MAX_LEAVES + 1))));
       __atomic_fetch_or(&configured, bit, __ATOMIC_ACQ_REL);
     }
     int sms = 148;
@@ -1231,8 +1266,12 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
     MKNN_LAUNCH k_chunk_base<<<1, PT_BUCKETS, 0, s>>>(st.bstart, ix.leaf_first, st.chunk, st.cbase);
     BucketLeaves bl{ix.leaf_first, ix.leaf_sub_base, st.cbase, st.cell_start, st.chunk_start,
                     st.box, st.chunk, n_leaves};
-    MKNN_LAUNCH k_bucket_sort<<<(unsigned)sms, BS_THREADS, smem, s>>>(st.rec, st.bstart, sstart, ix.bkey,
-                                                                       n_sub, n, st.kstart, st.obj, bl);
+    if (small)
+      MKNN_LAUNCH k_bucket_sort<512, BS_MAX_KEYS / 2, BS_MAX_LEAVES / 2><<<(unsigned)(2 * sms), 512, smem, s>>>(
+          st.rec, st.bstart, sstart, ix.bkey, n_sub, n, st.kstart, st.obj, bl);
+    else
+      MKNN_LAUNCH k_bucket_sort<1024, BS_MAX_KEYS, BS_MAX_LEAVES><<<(unsigned)sms, 1024, smem, s>>>(
+          st.rec, st.bstart, sstart, ix.bkey, n_sub, n, st.kstart, st.obj, bl);
     MKNN_CUDA_OK(cudaGetLastError());
     st.n_store = n;
     return 0;

@@ -187,8 +187,9 @@ int store_reserve(DevStore& st, int64_t n_sub, int64_t n_leaves, int64_t n);
 // outgrew its region (the caller redoes the tick with two_pass)
 int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const long long* ids,
                         const double* x, const double* y, int64_t n, int64_t n_leaves,
-                        int64_t n_sub, bool balanced, bool two_pass, unsigned long long* dev_clamped,
-                        unsigned long long* dev_overflow, void* scratch, cudaStream_t s);
+                        int64_t n_sub, bool balanced, int max_keys, int max_leaves, bool two_pass,
+                        unsigned long long* dev_clamped, unsigned long long* dev_overflow,
+                        void* scratch, cudaStream_t s);
 // Delta tick over the snapshot (sids/sx/sy, n_new slots): moved[0, m) are
 // the slots whose position changed (or were appended) since the store was
 // built from that snapshot.  dev_clamped_total: persistent count of objects

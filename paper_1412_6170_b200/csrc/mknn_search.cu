@@ -252,7 +252,8 @@ __device__ __forceinline__ void list_kth(const List<KPL>& L, int k, double& kd, 
 enum {
   PROF_OWN_CHUNKS_SCANNED, PROF_EXP_CHUNKS_SCANNED, PROF_INSERTS, PROF_SORT_MERGES,
   PROF_EXP_LEAF_VISITS, PROF_OWN_CHUNKS_TOTAL, PROF_EXP_CHUNKS_TOTAL, PROF_ADMITTED,
-  PROF_EXP_VISITS_NO_SCAN, PROF_EXP_VISITS_ADMITTING, PROF_N
+  PROF_EXP_VISITS_NO_SCAN, PROF_EXP_VISITS_ADMITTING, PROF_ROUNDS, PROF_ROUND_LANES,
+  PROF_NAV_STEPS, PROF_NAV_MAXSTEPS, PROF_N
 };
 #ifndef MKNN_PROFILE
 #define MKNN_PROFILE 0
@@ -858,13 +859,15 @@ __device__ __noinline__ bool audit_quadrant(const int32_t* __restrict__ z_map,
 __device__ __forceinline__ int navigate(const SearchArgs& a, int l_deep, int dir, int& cursor,
                                         double thr, double qx, double qy, long long me,
                                         uint32_t& prunes, uint32_t& viol,
-                                        const double2* __restrict__ cw) {
+                                        const double2* __restrict__ cw,
+                                        uint32_t* steps = nullptr) {
   const int n_codes = 1 << (2 * l_deep);
   int pos = cursor;
   if (dir ? pos >= n_codes : pos < 0) return -1;
   const bool full = thr < DINF;  // engine.py:415: thr = MAXDIST iff the list is full
   int lvl = full ? coarsest_level(pos, dir, l_deep) : l_deep;
   for (;;) {
+    if (MKNN_PROFILE && steps) (*steps)++;
     const int delta = l_deep - lvl;
     const uint32_t qc = (uint32_t)(pos >> (2 * delta));
     double md2 = 0.0;
@@ -1643,9 +1646,10 @@ __global__ void __launch_bounds__(32, MINB) k_search1(const __grid_constant__ Se
       const bool act = act_l || act_r;
       next_right = !go_right;
       int li = -1;
+      uint32_t nsteps = 0;
       if (act) {
         int cur = go_right ? cur_r : cur_l;
-        li = navigate(a, l_deep, go_right ? 1 : 0, cur, thr, qx, qy, me, prunes, viol, cw);
+        li = navigate(a, l_deep, go_right ? 1 : 0, cur, thr, qx, qy, me, prunes, viol, cw, &nsteps);
         if (go_right) {
           calls_r++;
           cur_r = cur;
@@ -1659,6 +1663,14 @@ __global__ void __launch_bounds__(32, MINB) k_search1(const __grid_constant__ Se
           emit_task(a, go_right ? 2 : 1, (go_right ? calls_r : calls_l) - 1, li);
           evals += (uint32_t)(__ldg(&a.cell_start[li + 1]) - __ldg(&a.cell_start[li]));
         }
+      }
+      if (MKNN_PROFILE && a.prof) {
+        const unsigned al = __ballot_sync(FULL, act);
+        const uint32_t mx = __reduce_max_sync(FULL, nsteps), sm = __reduce_add_sync(FULL, nsteps);
+        prof_add(a.prof, PROF_ROUNDS, 1, lane);
+        prof_add(a.prof, PROF_ROUND_LANES, __popc(al), lane);
+        prof_add(a.prof, PROF_NAV_STEPS, sm, lane);
+        prof_add(a.prof, PROF_NAV_MAXSTEPS, mx, lane);
       }
       // update_nn_lists: merge each assigned leaf into its query's list
       unsigned pend = __ballot_sync(FULL, li >= 0);
