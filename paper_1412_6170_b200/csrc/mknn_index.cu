@@ -177,7 +177,9 @@ __global__ void k_point_keys(const double* __restrict__ x, const double* __restr
                              unsigned long long* clamped, int bshift,
                              int32_t* __restrict__ bucket_cnt,
                              const uint16_t* __restrict__ leaf_bucket = nullptr,
-                             uint16_t* __restrict__ bkt_out = nullptr) {
+                             uint16_t* __restrict__ bkt_out = nullptr, int kshift = 0) {
+  // kshift: key_out and cnt take the sub-cell key >> kshift (the query
+  // counting sort groups 2^kshift consecutive sub-cells)
   // every key is counted in cnt; bucket_cnt != nullptr also counts the coarse
   // buckets (key >> bshift) of the store partition through a block histogram
   __shared__ int bh[PT_BUCKETS];
@@ -206,8 +208,8 @@ __global__ void k_point_keys(const double* __restrict__ x, const double* __restr
         uint32_t leaf, key;
         point_key(xi[u], yi[u], r, l_deep, info, leaf, key);
         if (leaf_out) leaf_out[i] = leaf;
-        key_out[i] = key;
-        if (cnt) atomicAdd(&cnt[key], 1);
+        key_out[i] = key >> kshift;
+        if (cnt) atomicAdd(&cnt[key >> kshift], 1);
         if (bucket_cnt) {
           int b = (int)(key >> bshift);
           if (leaf_bucket) {
@@ -1351,10 +1353,18 @@ int queries_index(DevQueries& dq, DevStore& st, const DevIndex& ix, const Region
                   cudaStream_t s) {
   *bits_used = 0;
   if (nq == 0) return 0;
+  // leaf-grouped order with sub-cell order inside (consecutive queries are
+  // neighbours: the own-pass cap and L1): a counting sort over groups of
+  // 2^qs consecutive sub-cells, about one query per group, so the scan
+  // covers n_sub >> qs entries instead of every sub-cell (cfg3: 15M -> 1.9M)
+  int qs = 0;
+  while (qs < 8 && (n_sub >> (qs + 1)) >= std::max<int64_t>(nq, 1)) qs++;
+  const int64_t n_grp = ((n_sub - 1) >> qs) + 1;
   MKNN_LAUNCH k_point_keys<<<grid_stride_blocks(nq), TPB, 0, s>>>(
-      qx, qy, nq, r, ix.scalars, ix.cell_info, dq.leaf, dq.qkey, st.qcnt, nullptr, 0, nullptr);
+      qx, qy, nq, r, ix.scalars, ix.cell_info, dq.leaf, dq.qkey, st.qcnt, nullptr, 0, nullptr,
+      nullptr, nullptr, qs);
   MKNN_CUDA_OK(cudaGetLastError());
-  int rc = exclusive_scan_i32(st.qcnt, st.qkstart, n_sub, scratch, s);
+  int rc = exclusive_scan_i32(st.qcnt, st.qkstart, n_grp, scratch, s);
   if (rc) return rc;
   MKNN_LAUNCH k_q_scatter<<<grid_stride_blocks(nq), TPB, 0, s>>>(nq, dq.qkey, st.qkstart, st.qcnt,
                                                                 dq.order);
