@@ -190,9 +190,9 @@ int64_t us_between(cudaEvent_t a, cudaEvent_t b) {
 
 }  // namespace
 
-// host-output ticks of >= SLICE_MIN_QUERIES queries search in N_SLICES
+// host-output ticks of >= SLICE_MIN_QUERIES queries search in n_slices
 // result-row slices whose copies to the host overlap the next slice
-constexpr int N_SLICES = 4;
+constexpr int MAX_SLICES = 16;
 constexpr int64_t SLICE_MIN_QUERIES = 65536;
 
 // pinned landing block of a tick's small device->host readbacks
@@ -220,7 +220,7 @@ struct mknn_engine {
   int issuer_bits = -1;        // issuer-id bits of the last tick (plans the row sort)
   bool issuer_dups = false;    // a batch repeated an issuer id: rows by radix sort from then on
   cudaStream_t copy_stream = nullptr;  // result slices device -> host
-  cudaEvent_t slice_ev[N_SLICES] = {};
+  cudaEvent_t slice_ev[MAX_SLICES] = {};
   cudaEvent_t q_ready = nullptr;  // host query batch staged on copy_stream
   PinBlock* pin = nullptr;
   bool q_pending = false;
@@ -696,6 +696,12 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
         a.task_cap = h->cap_tk;
       }
       sliced = sink && nq >= SLICE_MIN_QUERIES;
+      // MKNN_SLICES=n (<= 16): result-row slices of a host tick (A/B)
+      static const int n_slices = [] {
+        const char* e = getenv("MKNN_SLICES");
+        const int v = e ? atoi(e) : 4;
+        return v < 1 ? 1 : (v > MAX_SLICES ? MAX_SLICES : v);
+      }();
       h->rows_in_host = false;
       if (!sliced) {
         if ((rc = search_launch(a, s))) return h->set_err(rc);
@@ -705,7 +711,7 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
         // the leaf order (one 8-bit radix pass), then slice j's rows are copied
         // out while slice j + 1 searches
         MKNN_LAUNCH k_slice_keys<<<(unsigned)((nq + 255) / 256), 256, 0, s>>>(
-            h->dq.order, h->dq.row, nq, N_SLICES, h->dq.keys, h->dq.vals);
+            h->dq.order, h->dq.row, nq, n_slices, h->dq.keys, h->dq.vals);
         bool alt = false;
         if ((rc = radix_sort_pairs_u64(h->dq.keys, h->dq.vals, h->dq.keys_alt, h->dq.vals_alt, nq, 8,
                                        h->scratch.p, s, &alt)))
@@ -717,9 +723,9 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
           MKNN_CUDA_OK(cudaMemcpyAsync(sink->qids, o.qids, sizeof(int64_t) * nq, cudaMemcpyDeviceToHost,
                                        h->copy_stream));
         }
-        for (int j = 0; j < N_SLICES; j++) {
-          const int64_t r0 = (j * nq + N_SLICES - 1) / N_SLICES;
-          const int64_t r1 = ((j + 1) * nq + N_SLICES - 1) / N_SLICES;
+        for (int j = 0; j < n_slices; j++) {
+          const int64_t r0 = (j * nq + n_slices - 1) / n_slices;
+          const int64_t r1 = ((j + 1) * nq + n_slices - 1) / n_slices;
           if (r1 <= r0) continue;
           SearchArgs aj = a;
           aj.q_order = sorder + r0;
@@ -1247,7 +1253,7 @@ int mknn_create(const mknn_config* cfg, mknn_engine** out) {
   if (!rc && cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking) != cudaSuccess) rc = E_CUDA;
   for (int i = 0; i < 8 && !rc; i++)
     if (cudaEventCreate(&h->ev[i]) != cudaSuccess) rc = E_CUDA;
-  for (int i = 0; i < N_SLICES && !rc; i++)
+  for (int i = 0; i < MAX_SLICES && !rc; i++)
     if (cudaEventCreateWithFlags(&h->slice_ev[i], cudaEventDisableTiming) != cudaSuccess) rc = E_CUDA;
   if (!rc && cudaEventCreateWithFlags(&h->q_ready, cudaEventDisableTiming) != cudaSuccess)
     rc = E_CUDA;
