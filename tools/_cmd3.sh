@@ -1,2 +1,5 @@
-WLS="gaussian 1e7 1e6 32|uniform 1e7 1e6 32|uniform 1e6 1e5 32|uniform 1e8 1e7 16" VARS="MKNN_BSORT_BIG=0 MKNN_BSORT_BIG=1" bash tools/gpu_ab2.sh bs2
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_bs2.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_bs2.log; tail -2 gpurun_out/pytest_bs2.log
+mkdir -p gpurun_out
+for tool in memcheck racecheck synccheck; do
+  timeout 1200 compute-sanitizer --tool $tool --print-limit 10 python tools/sanitize_case.py > gpurun_out/san_$tool.log 2>&1
+  echo "== $tool rc=$?"; grep -E "ERROR SUMMARY|RACECHECK SUMMARY|ok" gpurun_out/san_$tool.log | tail -8
+done
