@@ -329,13 +329,21 @@ struct HostSink {
   double* dist;
 };
 
+struct SliceBounds {  // result-row slice j = rows [b[j], b[j + 1])
+  int64_t b[17];
+  int n;
+};
+
 __global__ void k_slice_keys(const uint32_t* __restrict__ order, const uint32_t* __restrict__ row,
-                             int64_t nq, int n_slices, uint64_t* __restrict__ keys,
+                             int64_t nq, const SliceBounds sb, uint64_t* __restrict__ keys,
                              uint32_t* __restrict__ vals) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < nq) {
     const uint32_t q = order[i];
-    keys[i] = (uint64_t)row[q] * (uint64_t)n_slices / (uint64_t)nq;
+    const int64_t r = row[q];
+    int j = 0;
+    while (j + 1 < sb.n && r >= sb.b[j + 1]) j++;
+    keys[i] = (uint64_t)j;
     vals[i] = q;
   }
 }
@@ -710,8 +718,28 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
         // j holds rows [ceil(j nq / S), ceil((j + 1) nq / S)), each slice keeps
         // the leaf order (one 8-bit radix pass), then slice j's rows are copied
         // out while slice j + 1 searches
+        // slice sizes grow geometrically (x4): the first slice's rows reach
+        // the host after a short search, and each later slice searches
+        // (~4.5x faster than PCIe carries its rows) while the previous one
+        // is copied, so the device->host link stays busy from the first
+        // slice on; MKNN_SLICE_GEO=0: equal slices (A/B)
+        static const bool geo = [] {
+          const char* e = getenv("MKNN_SLICE_GEO");
+          return !(e && e[0] == '0');
+        }();
+        SliceBounds sb{};
+        sb.n = n_slices;
+        double tot = 0.0, w = 1.0;
+        for (int j = 0; j < n_slices; j++, w *= (geo ? 4.0 : 1.0)) tot += w;
+        double acc = 0.0;
+        w = 1.0;
+        for (int j = 0; j <= n_slices; j++) {
+          sb.b[j] = j == n_slices ? nq : (int64_t)((double)nq * acc / tot);
+          if (j < n_slices) acc += w;
+          w *= geo ? 4.0 : 1.0;
+        }
         MKNN_LAUNCH k_slice_keys<<<(unsigned)((nq + 255) / 256), 256, 0, s>>>(
-            h->dq.order, h->dq.row, nq, n_slices, h->dq.keys, h->dq.vals);
+            h->dq.order, h->dq.row, nq, sb, h->dq.keys, h->dq.vals);
         bool alt = false;
         if ((rc = radix_sort_pairs_u64(h->dq.keys, h->dq.vals, h->dq.keys_alt, h->dq.vals_alt, nq, 8,
                                        h->scratch.p, s, &alt)))
@@ -724,8 +752,8 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
                                        h->copy_stream));
         }
         for (int j = 0; j < n_slices; j++) {
-          const int64_t r0 = (j * nq + n_slices - 1) / n_slices;
-          const int64_t r1 = ((j + 1) * nq + n_slices - 1) / n_slices;
+          const int64_t r0 = sb.b[j];
+          const int64_t r1 = sb.b[j + 1];
           if (r1 <= r0) continue;
           SearchArgs aj = a;
           aj.q_order = sorder + r0;
