@@ -142,13 +142,16 @@ __global__ void k_update_apply(const long long* __restrict__ ids, const double* 
                                const double* __restrict__ y, int64_t nu,
                                const int32_t* __restrict__ slot_of, int32_t* winner,
                                long long* sids, double* sx, double* sy, int32_t* mark,
-                               int32_t epoch, int32_t* moved, int32_t* n_moved, bool track) {
+                               int32_t epoch, int32_t* moved, int32_t* n_moved, bool track,
+                               const int32_t* __restrict__ n_before) {
+  // slots below the snapshot size before this batch already hold their id
+  const int32_t nb = *n_before;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nu;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t s = slot_of[i];
     bool first = false;
     if (winner[s] == (int32_t)i) {
-      sids[s] = ids[i];
+      if (s >= nb) sids[s] = ids[i];
       sx[s] = x[i];
       sy[s] = y[i];
       // slots changed since the store was built (once per slot and epoch)
@@ -1142,9 +1145,9 @@ int snap_reserve(mknn_engine* h, int64_t want) {
   h->st.valid = false;  // moved-slot history lost
   h->hcap = hc;
   h->cap_winner = nc;
-  if (!h->d_nsnap) {
-    MKNN_CUDA_OK(cudaMalloc(&h->d_nsnap, sizeof(int32_t)));
-    MKNN_CUDA_OK(cudaMemsetAsync(h->d_nsnap, 0, sizeof(int32_t), s));
+  if (!h->d_nsnap) {  // [0] the snapshot size, [1] its value before the current update batch
+    MKNN_CUDA_OK(cudaMalloc(&h->d_nsnap, 2 * sizeof(int32_t)));
+    MKNN_CUDA_OK(cudaMemsetAsync(h->d_nsnap, 0, 2 * sizeof(int32_t), s));
   }
   MKNN_LAUNCH k_fill_slots<<<gs_blocks(hc), 256, 0, s>>>(h->ht, hc);
   MKNN_LAUNCH k_fill_i32<<<gs_blocks(nc), 256, 0, s>>>(h->winner, nc, -1);
@@ -1210,6 +1213,7 @@ int snap_update_dev(mknn_engine* h, int64_t nu, const long long* ids, const doub
   }
   if ((rc = grow(h->slot_of, h->cap_slot_of, nu))) return rc;
   cudaStream_t s = h->stream;
+  MKNN_CUDA_OK(cudaMemcpyAsync(h->d_nsnap + 1, h->d_nsnap, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
   MKNN_LAUNCH k_update_claim<<<gs_blocks(nu), 256, 0, s>>>(ids, nu, h->ht, (uint64_t)(h->hcap - 1),
                                                h->d_nsnap, h->winner, h->slot_of);
   // a batch above the incremental threshold on its own (engine: > 5 % of
@@ -1220,7 +1224,7 @@ int snap_update_dev(mknn_engine* h, int64_t nu, const long long* ids, const doub
   if (!track) h->st.valid = false;
   MKNN_LAUNCH k_update_apply<<<gs_blocks(nu), 256, 0, s>>>(ids, x, y, nu, h->slot_of, h->winner, h->snap_ids,
                                                h->snap_x, h->snap_y, h->mark, h->epoch, h->moved,
-                                               h->d_nmoved, track);
+                                               h->d_nmoved, track, h->d_nsnap + 1);
   MKNN_LAUNCH k_update_reset<<<gs_blocks(nu), 256, 0, s>>>(nu, h->slot_of, h->winner);
   MKNN_CUDA_OK(cudaGetLastError());
   h->upd_pending = true;
