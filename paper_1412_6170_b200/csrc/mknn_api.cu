@@ -223,6 +223,12 @@ struct mknn_engine {
   int issuer_bits = -1;        // issuer-id bits of the last tick (plans the row sort)
   bool issuer_dups = false;    // a batch repeated an issuer id: rows by radix sort from then on
   cudaStream_t copy_stream = nullptr;  // result slices device -> host
+  // host ticks: the objects cross PCIe in chunks on in_stream while the
+  // one-pass partition of the chunks already copied runs on the main stream
+  cudaStream_t in_stream = nullptr;
+  cudaEvent_t in_ev[4] = {};
+  unsigned long long* pre_counts = nullptr;  // clamped, overflow of that partition
+  bool prepartitioned = false;
   cudaEvent_t slice_ev[MAX_SLICES] = {};
   cudaEvent_t q_ready = nullptr;  // host query batch staged on copy_stream
   PinBlock* pin = nullptr;
@@ -626,10 +632,11 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
       } else {
         if ((rc = store_index_objects(h->st, h->ix, h->r, ids, x, y, n, h->h_n_leaves, h->h_n_sub,
                                       h->h_bucket_load <= 4 * 16 && h->h_bucket_keys <= 32768,
-                                      (int)h->h_bucket_keys, (int)h->h_bucket_leaves, h->two_pass_next, h->counters + 3, h->counters + 4,
-                                      h->scratch.p,
-                                      s)))
+                                      (int)h->h_bucket_keys, (int)h->h_bucket_leaves, h->two_pass_next,
+                                      h->counters + 3, h->counters + 4, h->scratch.p, s,
+                                      h->prepartitioned ? h->pre_counts : nullptr)))
           return h->set_err(rc);
+        h->prepartitioned = false;  // a redo of the tick partitions again
         MKNN_CUDA_OK(cudaMemcpyAsync(h->clamped_total, h->counters + 3, sizeof(unsigned long long),
                                      cudaMemcpyDeviceToDevice, s));
       }
@@ -1078,7 +1085,8 @@ int host_out_tick(mknn_engine* h, int64_t n, const long long* ids, const double*
   return 0;
 }
 
-int stage_queries(mknn_engine* h, int64_t nq, const int64_t* qi, const double* qx, const double* qy) {
+int stage_queries(mknn_engine* h, int64_t nq, const int64_t* qi, const double* qx, const double* qy,
+                  cudaStream_t via = nullptr) {
   int rc;
   int64_t c = h->cap_qin;
   if ((rc = grow(h->in_qi, c, std::max<int64_t>(nq, 1)))) return rc;
@@ -1089,9 +1097,11 @@ int stage_queries(mknn_engine* h, int64_t nq, const int64_t* qi, const double* q
   h->cap_qin = c;
   // on the copy stream: the queries cross PCIe while the objects are
   // (re-)indexed; the tick waits for them just before index_queries
-  cudaStream_t cs = h->copy_stream;
-  MKNN_CUDA_OK(cudaEventRecord(h->ev[7], h->stream));  // inputs of the previous call consumed
-  MKNN_CUDA_OK(cudaStreamWaitEvent(cs, h->ev[7], 0));
+  cudaStream_t cs = via ? via : h->copy_stream;
+  if (!via) {  // (via: a stream already ordered after the previous call)
+    MKNN_CUDA_OK(cudaEventRecord(h->ev[7], h->stream));  // inputs of the previous call consumed
+    MKNN_CUDA_OK(cudaStreamWaitEvent(cs, h->ev[7], 0));
+  }
   if (nq) {
     MKNN_CUDA_OK(cudaMemcpyAsync(h->in_qi, qi, sizeof(int64_t) * nq, cudaMemcpyHostToDevice, cs));
     MKNN_CUDA_OK(cudaMemcpyAsync(h->in_qx, qx, sizeof(double) * nq, cudaMemcpyHostToDevice, cs));
@@ -1291,6 +1301,10 @@ int mknn_create(const mknn_config* cfg, mknn_engine** out) {
     rc = E_CUDA;
   if (!rc && cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
     rc = E_CUDA;
+  if (!rc && cudaStreamCreateWithFlags(&h->in_stream, cudaStreamNonBlocking) != cudaSuccess)
+    rc = E_CUDA;
+  for (auto& e : h->in_ev)
+    if (!rc && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) rc = E_CUDA;
   if (!rc && cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
     rc = E_CUDA;
   if (rc) {
@@ -1319,6 +1333,10 @@ void mknn_destroy(mknn_engine* h) {
   if (h->pin) cudaFreeHost(h->pin);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
+  if (h->in_stream) cudaStreamDestroy(h->in_stream);
+  for (auto& e : h->in_ev)
+    if (e) cudaEventDestroy(e);
+  if (h->pre_counts) cudaFree(h->pre_counts);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
 }
@@ -1356,12 +1374,54 @@ int mknn_tick(mknn_engine* h, int64_t n, const int64_t* ids, const double* x, co
   if ((rc = grow(h->in_y, c, std::max<int64_t>(n, 1)))) return h->set_err(rc);
   h->cap_in = c;
   cudaStream_t s = h->stream;
-  if (n) {
-    MKNN_CUDA_OK(cudaMemcpyAsync(h->in_ids, ids, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
-    MKNN_CUDA_OK(cudaMemcpyAsync(h->in_x, x, sizeof(double) * n, cudaMemcpyHostToDevice, s));
-    MKNN_CUDA_OK(cudaMemcpyAsync(h->in_y, y, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  // a steady-state tick that will take the one-pass partition (as
+  // core_tick_once decides: no rebuild, counts of the last bucket sort, no
+  // pending two-pass redo, balanced buckets) partitions each chunk of the
+  // objects as soon as it has crossed PCIe
+  static const bool overlap = [] {
+    const char* e = getenv("MKNN_H2D_OVERLAP");
+    const char* b = getenv("MKNN_BSORT");
+    const char* o = getenv("MKNN_ONEPASS");
+    return !(e && e[0] == '0') && !(b && b[0] == '0') && !(o && o[0] == '0');
+  }();
+  h->prepartitioned = false;
+  if (overlap && n >= (int64_t)1 << 20 && h->have_index && h->st.bcnt_valid && !h->two_pass_next &&
+      h->h_bucket_load <= 4 * 16 && h->h_bucket_keys <= 32768 &&
+      !should_rebuild(h->history, h->cfg.rebuild_window, h->cfg.rebuild_factor)) {
+    if ((rc = alloc_store(h, n))) return h->set_err(rc);
+    if ((rc = store_reserve(h->st, h->h_n_sub, h->h_n_leaves, n))) return h->set_err(rc);
+    if (!h->pre_counts) MKNN_CUDA_OK(cudaMalloc(&h->pre_counts, 2 * sizeof(unsigned long long)));
+    MKNN_CUDA_OK(cudaMemsetAsync(h->pre_counts, 0, 2 * sizeof(unsigned long long), s));
+    MKNN_CUDA_OK(cudaEventRecord(h->in_ev[3], s));  // the inputs of the previous tick are consumed
+    MKNN_CUDA_OK(cudaStreamWaitEvent(h->in_stream, h->in_ev[3], 0));
+    constexpr int C = 4;
+    for (int c = 0; c < C; c++) {
+      const int64_t lo = n * c / C, hi = n * (c + 1) / C;
+      cudaStream_t is = h->in_stream;
+      MKNN_CUDA_OK(cudaMemcpyAsync(h->in_ids + lo, ids + lo, sizeof(int64_t) * (hi - lo),
+                                   cudaMemcpyHostToDevice, is));
+      MKNN_CUDA_OK(cudaMemcpyAsync(h->in_x + lo, x + lo, sizeof(double) * (hi - lo),
+                                   cudaMemcpyHostToDevice, is));
+      MKNN_CUDA_OK(cudaMemcpyAsync(h->in_y + lo, y + lo, sizeof(double) * (hi - lo),
+                                   cudaMemcpyHostToDevice, is));
+      MKNN_CUDA_OK(cudaEventRecord(h->in_ev[c], is));
+      MKNN_CUDA_OK(cudaStreamWaitEvent(s, h->in_ev[c], 0));
+      if ((rc = store_prepartition(h->st, h->ix, h->r, h->in_ids, h->in_x, h->in_y, lo, hi, c == 0,
+                                   h->pre_counts, s)))
+        return h->set_err(rc);
+    }
+    h->prepartitioned = true;
+    // the queries follow the objects on the same stream: the link stays busy
+    // while the bucket sort runs
+    if ((rc = stage_queries(h, nq, q_issuer, qx, qy, h->in_stream))) return h->set_err(rc);
+  } else {
+    if (n) {
+      MKNN_CUDA_OK(cudaMemcpyAsync(h->in_ids, ids, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+      MKNN_CUDA_OK(cudaMemcpyAsync(h->in_x, x, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+      MKNN_CUDA_OK(cudaMemcpyAsync(h->in_y, y, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    }
+    if ((rc = stage_queries(h, nq, q_issuer, qx, qy))) return h->set_err(rc);
   }
-  if ((rc = stage_queries(h, nq, q_issuer, qx, qy))) return h->set_err(rc);
   return host_out_tick(h, n, h->in_ids, h->in_x, h->in_y, nq, h->in_qi, h->in_qx, h->in_qy,
                        out_qids, out_len, out_nids, out_dist, metrics, t0);
 }

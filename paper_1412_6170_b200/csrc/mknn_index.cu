@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(PT_THREADS) k_partition_keys(
     int64_t n, Region r, const int32_t* __restrict__ scalars,
     const unsigned long long* __restrict__ info, const uint16_t* __restrict__ leaf_bucket,
     const int32_t* __restrict__ sstart, int32_t* __restrict__ cursor, StoreRec* __restrict__ out,
-    unsigned long long* clamped, unsigned long long* overflow) {
+    unsigned long long* clamped, unsigned long long* overflow, int64_t index_base = 0) {
   __shared__ int hist[PT_BUCKETS], gbase[PT_BUCKETS];
   const int t = threadIdx.x;
   const int64_t base = (int64_t)blockIdx.x * PT_TILE;
@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(PT_THREADS) k_partition_keys(
       rc[j].x = x[i];
       rc[j].y = y[i];
       rc[j].id = ids[i];
-      rc[j].pad = (uint32_t)i;  // input index (the snapshot slot on the delta path)
+      rc[j].pad = (uint32_t)(index_base + i);  // input index (the snapshot slot on the delta path)
     }
   }
 #pragma unroll
@@ -1193,11 +1193,27 @@ static int store_finish(DevStore& st, const DevIndex& ix, int64_t n, int64_t n_l
   return 0;
 }
 
+// the one-pass partition of the objects [lo, hi) (plan: first call of a
+// tick: lay out the bucket regions); a host tick runs it per chunk while the
+// next chunk crosses PCIe, and store_index_objects then starts from the
+// partitioned records (pre != nullptr)
+int store_prepartition(DevStore& st, const DevIndex& ix, const Region& r, const long long* ids,
+                       const double* x, const double* y, int64_t lo, int64_t hi, bool plan,
+                       unsigned long long* pre, cudaStream_t s) {
+  if (plan) MKNN_LAUNCH k_cap_plan<<<1, PT_BUCKETS, 0, s>>>(st.bcnt, st.sstart, st.cursor);
+  if (hi > lo)
+    MKNN_LAUNCH k_partition_keys<<<(unsigned)((hi - lo + PT_TILE - 1) / PT_TILE), PT_THREADS, 0, s>>>(
+        ids + lo, x + lo, y + lo, hi - lo, r, ix.scalars, ix.cell_info, ix.leaf_bucket, st.sstart,
+        st.cursor, st.rec, pre, pre + 1, lo);
+  MKNN_CUDA_OK(cudaGetLastError());
+  return 0;
+}
+
 int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const long long* ids,
                         const double* x, const double* y, int64_t n, int64_t n_leaves,
                         int64_t n_sub, bool balanced, int max_keys, int max_leaves, bool two_pass,
                         unsigned long long* dev_clamped, unsigned long long* dev_overflow,
-                        void* scratch, cudaStream_t s) {
+                        void* scratch, cudaStream_t s, const unsigned long long* pre) {
   // MKNN_BSORT=0: the global-atomic counting sort (per-key counts in the
   // key pass, a scan over all sub-cells, an atomic final scatter) for A/B
   static const bool bsort = [] {
@@ -1224,10 +1240,17 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
     }();
     const int32_t* sstart = st.bstart;  // two-pass: staging and store share the layout
     if (onepass && st.bcnt_valid && !two_pass) {
-      MKNN_LAUNCH k_cap_plan<<<1, PT_BUCKETS, 0, s>>>(st.bcnt, st.sstart, st.cursor);
-      MKNN_LAUNCH k_partition_keys<<<(unsigned)((n + PT_TILE - 1) / PT_TILE), PT_THREADS, 0, s>>>(
-          ids, x, y, n, r, ix.scalars, ix.cell_info, ix.leaf_bucket, st.sstart, st.cursor, st.rec,
-          dev_clamped, dev_overflow);
+      if (pre) {  // partitioned while the objects arrived: take its counters
+        MKNN_CUDA_OK(cudaMemcpyAsync(dev_clamped, pre, sizeof(unsigned long long),
+                                     cudaMemcpyDeviceToDevice, s));
+        MKNN_CUDA_OK(cudaMemcpyAsync(dev_overflow, pre + 1, sizeof(unsigned long long),
+                                     cudaMemcpyDeviceToDevice, s));
+      } else {
+        MKNN_LAUNCH k_cap_plan<<<1, PT_BUCKETS, 0, s>>>(st.bcnt, st.sstart, st.cursor);
+        MKNN_LAUNCH k_partition_keys<<<(unsigned)((n + PT_TILE - 1) / PT_TILE), PT_THREADS, 0, s>>>(
+            ids, x, y, n, r, ix.scalars, ix.cell_info, ix.leaf_bucket, st.sstart, st.cursor, st.rec,
+            dev_clamped, dev_overflow);
+      }
       MKNN_LAUNCH k_bucket_counts<<<1, PT_BUCKETS, 0, s>>>(st.sstart, st.cursor, st.bcnt, st.bstart);
       sstart = st.sstart;
     } else {

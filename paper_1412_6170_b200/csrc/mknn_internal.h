@@ -189,7 +189,12 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
                         const double* x, const double* y, int64_t n, int64_t n_leaves,
                         int64_t n_sub, bool balanced, int max_keys, int max_leaves, bool two_pass,
                         unsigned long long* dev_clamped, unsigned long long* dev_overflow,
-                        void* scratch, cudaStream_t s);
+                        void* scratch, cudaStream_t s, const unsigned long long* pre = nullptr);
+// the one-pass partition of objects [lo, hi) ahead of store_index_objects
+// (pre: device u64[2], clamped and overflow accumulators, zeroed by the caller)
+int store_prepartition(DevStore& st, const DevIndex& ix, const Region& r, const long long* ids,
+                       const double* x, const double* y, int64_t lo, int64_t hi, bool plan,
+                       unsigned long long* pre, cudaStream_t s);
 // Delta tick over the snapshot (sids/sx/sy, n_new slots): moved[0, m) are
 // the slots whose position changed (or were appended) since the store was
 // built from that snapshot.  dev_clamped_total: persistent count of objects
