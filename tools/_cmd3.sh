@@ -1,2 +1,5 @@
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_upd2.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_upd2.log; tail -2 gpurun_out/pytest_upd2.log
-for wl in cfg4 cfg2; do timeout 900 python bench.py --workload $wl --steps 10 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/bu_$wl.json 2>/dev/null; python -c "import json;d=json.load(open('gpurun_out/bu_$wl.json'));p=d['tick_phases_us'];print('$wl', round(d['value']/1e6,1), round(d['ms_per_step'],3), p, round(d['ms_per_step']*1e3-sum(p.values())))"; done
+for cfg in "MKNN_H2D_OVERLAP=0" "MKNN_H2D_OVERLAP=1" "MKNN_H2D_OVERLAP=0" "MKNN_H2D_OVERLAP=1"; do
+  env $cfg timeout 600 python bench.py --steps 2 --warmup 3 --e2e-steps 6 --no-cpu-baseline > gpurun_out/bov.json 2>/dev/null
+  python -c "import json;d=json.load(open('gpurun_out/bov.json'));print('$cfg', round(d['value']/1e6,1), round(d['e2e']['value']/1e6,2))"
+done
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_ov.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_ov.log; tail -2 gpurun_out/pytest_ov.log
