@@ -209,6 +209,28 @@ struct PinBlock {
   uint32_t hist[2][HIST];
 };
 
+// every small readback of a tick, written straight into the mapped pinned
+// block by one kernel (one graph node instead of a chain of tiny copies)
+__global__ void k_readback(const unsigned long long* __restrict__ counters,
+                           const int64_t* __restrict__ minmax, const int64_t* __restrict__ total,
+                           const int32_t* __restrict__ dup, const int32_t* __restrict__ nsnap,
+                           const uint32_t* __restrict__ hist, int64_t hist_cap, int hpre,
+                           PinBlock* pb) {
+  const int t = threadIdx.x;
+  if (t < 8) pb->cnt[t] = counters[t];
+  if (t == 8) {
+    pb->mm[0] = minmax ? minmax[0] : 0;
+    pb->mm[1] = minmax ? minmax[1] : 0;
+  }
+  if (t == 9) pb->total = *total;
+  if (t == 10) pb->dup = dup ? *dup : 0;
+  if (t == 11) pb->nsnap = nsnap ? *nsnap : 0;
+  for (int i = t; i < hpre; i += blockDim.x) {
+    pb->hist[0][i] = hist[i];
+    pb->hist[1][i] = hist[hist_cap + i];
+  }
+}
+
 struct mknn_engine {
   mknn_config cfg{};
   Region r{};
@@ -232,6 +254,7 @@ struct mknn_engine {
   cudaEvent_t slice_ev[MAX_SLICES] = {};
   cudaEvent_t q_ready = nullptr;  // host query batch staged on copy_stream
   PinBlock* pin = nullptr;
+  PinBlock* pin_dev = nullptr;  // the same block as the device sees it (mapped)
   bool q_pending = false;
   bool rows_in_host = false;   // the sliced host tick already delivered qids/len/rows
   bool retry_rebuild = false;  // false: the store's sub-cell counters may be dirty
@@ -541,7 +564,10 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
                         radix_scratch_bytes(std::max<int64_t>(nq, 1))});
   if ((rc = h->scratch.ensure(sb + 1024))) return h->set_err(rc);
 
-  if (!h->pin) MKNN_CUDA_OK(cudaMallocHost(&h->pin, sizeof(PinBlock)));
+  if (!h->pin) {
+    MKNN_CUDA_OK(cudaHostAlloc(&h->pin, sizeof(PinBlock), cudaHostAllocMapped));
+    MKNN_CUDA_OK(cudaHostGetDevicePointer(&h->pin_dev, h->pin, 0));
+  }
 
   mknn_metrics m{};
   m.tick = h->tick;
@@ -809,21 +835,13 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
       MKNN_CUDA_OK(cudaEventRecordWithFlags(h->ev[5], s, ev_flags));
 
       prof_on = a.prof != nullptr;
-      // every small readback of the tick in one pinned block, one sync
-      PinBlock& pb = *h->pin;
-      MKNN_CUDA_OK(cudaMemcpyAsync(pb.cnt, h->counters, sizeof(pb.cnt), cudaMemcpyDeviceToHost, s));
-      pb.mm[0] = pb.mm[1] = 0;
-      if (nq) MKNN_CUDA_OK(cudaMemcpyAsync(pb.mm, h->dq.minmax, sizeof(pb.mm), cudaMemcpyDeviceToHost, s));
-      MKNN_CUDA_OK(cudaMemcpyAsync(&pb.total, o.offsets + nq, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-      pb.dup = 0;
-      if (h->n_spec >= 0)  // a tick on the unconfirmed snapshot size checks it
-        MKNN_CUDA_OK(cudaMemcpyAsync(&pb.nsnap, h->d_nsnap, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-      if (nq && h->dq.dup)
-        MKNN_CUDA_OK(cudaMemcpyAsync(&pb.dup, h->dq.dup, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-      if (nq)
-        for (int d = 0; d < 2; d++)
-          MKNN_CUDA_OK(cudaMemcpyAsync(pb.hist[d], h->hist + (int64_t)d * h->hist_cap,
-                                       sizeof(uint32_t) * hpre, cudaMemcpyDeviceToHost, s));
+      // every small readback of the tick into the pinned block (mapped: one
+      // kernel writes it), one sync; nsnap is checked on speculative ticks only
+      MKNN_LAUNCH k_readback<<<1, 256, 0, s>>>(h->counters, nq ? h->dq.minmax : nullptr, o.offsets + nq,
+                                               nq ? h->dq.dup : nullptr,
+                                               h->n_spec >= 0 ? h->d_nsnap : nullptr, h->hist,
+                                               h->hist_cap, nq ? (int)hpre : 0, h->pin_dev);
+      MKNN_CUDA_OK(cudaGetLastError());
       return 0;
     };
     erc = enqueue();
@@ -1197,7 +1215,10 @@ int snap_load_dev(mknn_engine* h, int64_t n, const long long* ids, const double*
 // the exact snapshot size and moved-slot count after sync-free updates
 int snap_sync(mknn_engine* h) {
   if (!h->upd_pending) return 0;
-  if (!h->pin) MKNN_CUDA_OK(cudaMallocHost(&h->pin, sizeof(PinBlock)));
+  if (!h->pin) {
+    MKNN_CUDA_OK(cudaHostAlloc(&h->pin, sizeof(PinBlock), cudaHostAllocMapped));
+    MKNN_CUDA_OK(cudaHostGetDevicePointer(&h->pin_dev, h->pin, 0));
+  }
   cudaStream_t s = h->stream;
   MKNN_CUDA_OK(cudaMemcpyAsync(&h->pin->nsnap, h->d_nsnap, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   MKNN_CUDA_OK(cudaMemcpyAsync(&h->pin->dup, h->d_nmoved, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
