@@ -341,6 +341,14 @@ __global__ void k_final_scatter(const StoreRec* __restrict__ rec, int64_t n,
 // the records of the second sweep are still in L2.
 constexpr int BS_MAX_KEYS = 32768;    // 128 KB shared key histogram per bucket
 constexpr int BS_MAX_LEAVES = 8192;   // leaves per bucket (two 32 KB leaf arrays)
+#ifndef MKNN_BS_U
+#define MKNN_BS_U 4
+#endif
+constexpr int BS_U = MKNN_BS_U;      // records in flight per thread in the sort's sweeps
+#ifndef MKNN_BS_G
+#define MKNN_BS_G 4
+#endif
+constexpr int BS_G = MKNN_BS_G;      // lanes per chunk in the sort's box phase
 
 // in-place exclusive scan of v[0, m) by the whole CTA, plus `base`;
 // returns the total (v[m] is not written)
@@ -391,7 +399,21 @@ struct BucketLeaves {  // the leaf side of k_bucket_sort (store_finish's passes,
   ChunkBox* box;              // out, per chunk slot
   int chunk;                  // objects per chunk
   int64_t n_leaves;
+  int prefetch;               // bulk-prefetch the next bucket's staged records into L2
 };
+
+// cp.async.bulk.prefetch.L2 of bucket b's staged records, in 32 KB pieces
+// spread over the lanes of one warp
+__device__ __forceinline__ void prefetch_bucket(const StoreRec* rec, const int32_t* sstart,
+                                                const int32_t* bstart, int b, int lane) {
+  if (b >= PT_BUCKETS) return;
+  const char* p = reinterpret_cast<const char*>(rec + sstart[b]);
+  const unsigned bytes = (unsigned)(bstart[b + 1] - bstart[b]) * (unsigned)sizeof(StoreRec);
+  for (unsigned o = (unsigned)lane * 32768u; o < bytes; o += 32u * 32768u) {
+    const unsigned sz = min(32768u, bytes - o);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p + o), "r"(sz) : "memory");
+  }
+}
 
 // Pass 2, bucket-local: one CTA sorts one partition bucket by sub-cell key
 // in shared memory -- no global atomics.  The bucket's records occupy
@@ -423,22 +445,47 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_bucket_sort(
     kstart[n_sub] = (int32_t)n;
     bl.cell_start[bl.n_leaves] = (int32_t)n;
   }
+  if (bl.prefetch && t < 32) prefetch_bucket(rec, sstart, bstart, blockIdx.x, t);
   for (int b = blockIdx.x; b < PT_BUCKETS; b += gridDim.x) {
+    // prefetch 1: the next bucket's records stream into L2 while this one
+    // is sorted; 2: only once this bucket's records are placed
+    if (bl.prefetch == 1 && t < 32) prefetch_bucket(rec, sstart, bstart, b + gridDim.x, t);
     const int kb = bkey[b];
     const int nk = bkey[b + 1] - kb;  // <= MK (checked at the rebuild)
     const int bs = bstart[b], be = bstart[b + 1];
     const StoreRec* __restrict__ src = rec + (sstart[b] - bs);  // src[i] for i in [bs, be)
     for (int j = t; j < nk; j += NT) hist[j] = 0;
     __syncthreads();
-    for (int i = bs + t; i < be; i += NT) atomicAdd(&hist[(int)__ldg(&src[i].key) - kb], 1);
+    // both sweeps issue BS_U loads before their shared atomics (one record
+    // per thread per step left each warp one load in flight)
+    int i = bs + t;
+    for (; i + (BS_U - 1) * NT < be; i += BS_U * NT) {
+      uint32_t kk[BS_U];
+#pragma unroll
+      for (int u = 0; u < BS_U; u++) kk[u] = __ldg(&src[i + u * NT].key);
+#pragma unroll
+      for (int u = 0; u < BS_U; u++) atomicAdd(&hist[(int)kk[u] - kb], 1);
+    }
+    for (; i < be; i += NT) atomicAdd(&hist[(int)__ldg(&src[i].key) - kb], 1);
     __syncthreads();
     block_exclusive_scan<NT>(hist, nk, bs, wsum);
     for (int j = t; j < nk; j += NT) kstart[kb + j] = hist[j];
     __syncthreads();
-    for (int i = bs + t; i < be; i += NT) {
+    for (i = bs + t; i + (BS_U - 1) * NT < be; i += BS_U * NT) {
+      StoreRec rr[BS_U];
+      int pp[BS_U];
+#pragma unroll
+      for (int u = 0; u < BS_U; u++) rr[u] = ld_rec(&src[i + u * NT]);
+#pragma unroll
+      for (int u = 0; u < BS_U; u++) pp[u] = atomicAdd(&hist[(int)rr[u].key - kb], 1);
+#pragma unroll
+      for (int u = 0; u < BS_U; u++) st_rec(&obj[pp[u]], rr[u]);
+    }
+    for (; i < be; i += NT) {
       const StoreRec r = ld_rec(&src[i]);
       st_rec(&obj[atomicAdd(&hist[(int)r.key - kb], 1)], r);
     }
+    if (bl.prefetch == 2 && t < 32) prefetch_bucket(rec, sstart, bstart, b + gridDim.x, t);
     __syncthreads();
     // hist[j] is now the end of key j: a leaf starts where its first key does
     const int lf = bl.leaf_first[b], nlb = bl.leaf_first[b + 1] - lf;  // <= ML
@@ -456,24 +503,40 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_bucket_sort(
     for (int l = t; l < nlb; l += NT) bl.chunk_start[lf + l] = cb + lpre[l];
     if (t == 0) lpre[nlb] = nchunks;
     __syncthreads();
-    for (int q = t; q < nchunks; q += NT) {
-      int lo = 0, hi = nlb;  // the leaf: lpre[lo] <= q < lpre[lo + 1]
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (lpre[mid] <= q) lo = mid; else hi = mid;
-      }
-      const int o0 = lcs[lo] + (q - lpre[lo]) * bl.chunk;
-      const int oe = lo + 1 < nlb ? lcs[lo + 1] : be;
-      const int o1 = min(o0 + bl.chunk, oe);
+    // BS_G lanes per chunk, each reading every BS_G-th record (coalesced
+    // runs, all of a lane's loads in flight), then a shuffle reduction
+    for (int q0 = 0; q0 < nchunks; q0 += NT / BS_G) {
+      const int q = q0 + t / BS_G, g = t & (BS_G - 1);
       double xl = DINF, yl = DINF, xh = -DINF, yh = -DINF;
-      for (int o = o0; o < o1; o++) {
-        const double2 p = *reinterpret_cast<const double2*>(&obj[o]);
-        xl = fmin(xl, p.x);
-        xh = fmax(xh, p.x);
-        yl = fmin(yl, p.y);
-        yh = fmax(yh, p.y);
+      if (q < nchunks) {
+        int lo = 0, hi = nlb;  // the leaf: lpre[lo] <= q < lpre[lo + 1]
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (lpre[mid] <= q) lo = mid; else hi = mid;
+        }
+        const int o0 = lcs[lo] + (q - lpre[lo]) * bl.chunk;
+        const int oe = lo + 1 < nlb ? lcs[lo + 1] : be;
+        const int o1 = min(o0 + bl.chunk, oe);
+#pragma unroll
+        for (int u = 0; u < MAX_CHUNK / BS_G; u++) {
+          const int o = o0 + g + u * BS_G;
+          if (o < o1) {
+            const double2 p = *reinterpret_cast<const double2*>(&obj[o]);
+            xl = fmin(xl, p.x);
+            xh = fmax(xh, p.x);
+            yl = fmin(yl, p.y);
+            yh = fmax(yh, p.y);
+          }
+        }
       }
-      bl.box[cb + q] = ChunkBox{xl, yl, xh, yh};
+#pragma unroll
+      for (int o = 1; o < BS_G; o <<= 1) {
+        xl = fmin(xl, __shfl_xor_sync(FULL, xl, o));
+        xh = fmax(xh, __shfl_xor_sync(FULL, xh, o));
+        yl = fmin(yl, __shfl_xor_sync(FULL, yl, o));
+        yh = fmax(yh, __shfl_xor_sync(FULL, yh, o));
+      }
+      if (q < nchunks && g == 0) bl.box[cb + q] = ChunkBox{xl, yl, xh, yh};
     }
     __syncthreads();
   }
@@ -1289,8 +1352,13 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
     int sms = 148;
     MKNN_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     MKNN_LAUNCH k_chunk_base<<<1, PT_BUCKETS, 0, s>>>(st.bstart, ix.leaf_first, st.chunk, st.cbase);
+    // MKNN_BS_PREFETCH=1|2: bulk L2 prefetch of the next bucket (A/B)
+    static const int prefetch = [] {
+      const char* e = getenv("MKNN_BS_PREFETCH");
+      return e ? atoi(e) : 0;
+    }();
     BucketLeaves bl{ix.leaf_first, ix.leaf_sub_base, st.cbase, st.cell_start, st.chunk_start,
-                    st.box, st.chunk, n_leaves};
+                    st.box, st.chunk, n_leaves, prefetch};
     if (small)
       MKNN_LAUNCH k_bucket_sort<512, BS_MAX_KEYS / 2, BS_MAX_LEAVES / 2><<<(unsigned)(2 * sms), 512, smem, s>>>(
           st.rec, st.bstart, sstart, ix.bkey, n_sub, n, st.kstart, st.obj, bl);

@@ -343,7 +343,20 @@ __global__ void k_minmax(const int64_t* __restrict__ in, int64_t n, int64_t* out
     lo = a < lo ? a : lo;
     hi = b > hi ? b : hi;
   }
+  // one atomic pair per block: same-address L2 atomics serialise, and one
+  // per warp (9.5K at 1M queries) cost more than the loads
+  __shared__ long long wlo[32], whi[32];
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if ((threadIdx.x & 31) == 0) {
+    wlo[w] = lo;
+    whi[w] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 1; j < nw; j++) {
+      lo = wlo[j] < lo ? wlo[j] : lo;
+      hi = whi[j] > hi ? whi[j] : hi;
+    }
     atomicMin((long long*)&out[0], lo);
     atomicMax((long long*)&out[1], hi);
   }

@@ -1914,12 +1914,20 @@ __global__ void k_stats_reduce(const QueryStats* __restrict__ st, int64_t nq,
     pr += __shfl_xor_sync(FULL, pr, o);
     vi += __shfl_xor_sync(FULL, vi, o);
   }
+  // one atomic per counter and block (same-address L2 atomics serialise)
+  __shared__ unsigned long long wt[3][32];
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if ((threadIdx.x & 31) == 0) {
-    if (ev) atomicAdd(&tot[0], ev);
-    if (pr) atomicAdd(&tot[1], pr);
-    if (vi) atomicAdd(&tot[2], vi);
+    wt[0][w] = ev;
+    wt[1][w] = pr;
+    wt[2][w] = vi;
   }
   __syncthreads();
+  if (threadIdx.x < 3) {
+    unsigned long long v = 0;
+    for (int j = 0; j < nw; j++) v += wt[threadIdx.x][j];
+    if (v) atomicAdd(&tot[threadIdx.x], v);
+  }
   for (int i = threadIdx.x; i < HIST_SMEM && i < hist_cap; i += blockDim.x) {
     if (hl[i]) atomicAdd(&hist_l[i], hl[i]);
     if (hr[i]) atomicAdd(&hist_r[i], hr[i]);
