@@ -351,43 +351,78 @@ constexpr int BS_U = MKNN_BS_U;      // records in flight per thread in the sort
 constexpr int BS_G = MKNN_BS_G;      // lanes per chunk in the sort's box phase
 
 // in-place exclusive scan of v[0, m) by the whole CTA, plus `base`;
-// returns the total (v[m] is not written)
+// returns the total (v[m] is not written).  Each warp owns a contiguous
+// segment and walks it in rows of 32 (lane j reads element j of the row:
+// no bank conflicts, where one contiguous run per thread conflicted E-way)
 template <int NT>
 __device__ __forceinline__ int block_exclusive_scan(int32_t* v, int m, int base, int32_t* wsum) {
+  constexpr int NW = NT / 32;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int E = (m + NT - 1) / NT;
-  const int j0 = min(t * E, m), j1 = min(j0 + E, m);
+  const int seg = (((m + NW - 1) / NW) + 31) & ~31;
+  const int s0 = min(w * seg, m), s1 = min(s0 + seg, m);
   int sum = 0;
-  for (int j = j0; j < j1; j++) sum += v[j];
-  int inc = sum;
+  for (int j = s0 + lane; j < s1; j += 32) sum += v[j];
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int u = __shfl_up_sync(FULL, inc, o);
-    if (lane >= o) inc += u;
-  }
-  if (lane == 31) wsum[w] = inc;
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+  if (lane == 0) wsum[w] = sum;
   __syncthreads();
   if (w == 0) {
-    const int x = lane < NT / 32 ? wsum[lane] : 0;
+    const int x = lane < NW ? wsum[lane] : 0;
     int xi = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int u = __shfl_up_sync(FULL, xi, o);
       if (lane >= o) xi += u;
     }
-    if (lane < NT / 32) wsum[lane] = xi - x;
-    if (lane == 31) wsum[NT / 32] = xi;  // the total
+    if (lane < NW) wsum[lane] = xi - x;
+    if (lane == 31) wsum[NW] = xi;  // the total
   }
   __syncthreads();
-  int run = base + wsum[w] + inc - sum;
-  for (int j = j0; j < j1; j++) {
-    const int c = v[j];
-    v[j] = run;
-    run += c;
+  int carry = base + wsum[w];
+  for (int j0 = s0; j0 < s1; j0 += 32) {
+    const int j = j0 + lane;
+    const int c = j < s1 ? v[j] : 0;
+    int inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(FULL, inc, o);
+      if (lane >= o) inc += u;
+    }
+    if (j < s1) v[j] = carry + inc - c;
+    carry += __shfl_sync(FULL, inc, 31);
   }
-  const int total = wsum[NT / 32];
+  const int total = wsum[NW];
   __syncthreads();
   return total;
+}
+
+// one step of k_bucket_sort's sweeps: U records per thread, NT apart
+template <int U, int NT, bool GUARD>
+__device__ __forceinline__ void count_step(const StoreRec* __restrict__ src, int i, int be,
+                                           int32_t* hist, int kb) {
+  uint32_t kk[U];
+#pragma unroll
+  for (int u = 0; u < U; u++)
+    if (!GUARD || i + u * NT < be) kk[u] = __ldg(&src[i + u * NT].key);
+#pragma unroll
+  for (int u = 0; u < U; u++)
+    if (!GUARD || i + u * NT < be) atomicAdd(&hist[(int)kk[u] - kb], 1);
+}
+
+template <int U, int NT, bool GUARD>
+__device__ __forceinline__ void place_step(const StoreRec* __restrict__ src, int i, int be,
+                                           int32_t* hist, int kb, StoreRec* __restrict__ obj) {
+  StoreRec rr[U];
+  int pp[U];
+#pragma unroll
+  for (int u = 0; u < U; u++)
+    if (!GUARD || i + u * NT < be) rr[u] = ld_rec(&src[i + u * NT]);
+#pragma unroll
+  for (int u = 0; u < U; u++)
+    if (!GUARD || i + u * NT < be) pp[u] = atomicAdd(&hist[(int)rr[u].key - kb], 1);
+#pragma unroll
+  for (int u = 0; u < U; u++)
+    if (!GUARD || i + u * NT < be) st_rec(&obj[pp[u]], rr[u]);
 }
 
 struct BucketLeaves {  // the leaf side of k_bucket_sort (store_finish's passes, fused)
@@ -457,34 +492,18 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_bucket_sort(
     for (int j = t; j < nk; j += NT) hist[j] = 0;
     __syncthreads();
     // both sweeps issue BS_U loads before their shared atomics (one record
-    // per thread per step left each warp one load in flight)
+    // per thread per step left each warp one load in flight); the last
+    // partial step is predicated rather than a one-record tail loop
     int i = bs + t;
-    for (; i + (BS_U - 1) * NT < be; i += BS_U * NT) {
-      uint32_t kk[BS_U];
-#pragma unroll
-      for (int u = 0; u < BS_U; u++) kk[u] = __ldg(&src[i + u * NT].key);
-#pragma unroll
-      for (int u = 0; u < BS_U; u++) atomicAdd(&hist[(int)kk[u] - kb], 1);
-    }
-    for (; i < be; i += NT) atomicAdd(&hist[(int)__ldg(&src[i].key) - kb], 1);
+    for (; i + (BS_U - 1) * NT < be; i += BS_U * NT) count_step<BS_U, NT, false>(src, i, be, hist, kb);
+    if (i < be) count_step<BS_U, NT, true>(src, i, be, hist, kb);
     __syncthreads();
     block_exclusive_scan<NT>(hist, nk, bs, wsum);
     for (int j = t; j < nk; j += NT) kstart[kb + j] = hist[j];
     __syncthreads();
-    for (i = bs + t; i + (BS_U - 1) * NT < be; i += BS_U * NT) {
-      StoreRec rr[BS_U];
-      int pp[BS_U];
-#pragma unroll
-      for (int u = 0; u < BS_U; u++) rr[u] = ld_rec(&src[i + u * NT]);
-#pragma unroll
-      for (int u = 0; u < BS_U; u++) pp[u] = atomicAdd(&hist[(int)rr[u].key - kb], 1);
-#pragma unroll
-      for (int u = 0; u < BS_U; u++) st_rec(&obj[pp[u]], rr[u]);
-    }
-    for (; i < be; i += NT) {
-      const StoreRec r = ld_rec(&src[i]);
-      st_rec(&obj[atomicAdd(&hist[(int)r.key - kb], 1)], r);
-    }
+    for (i = bs + t; i + (BS_U - 1) * NT < be; i += BS_U * NT)
+      place_step<BS_U, NT, false>(src, i, be, hist, kb, obj);
+    if (i < be) place_step<BS_U, NT, true>(src, i, be, hist, kb, obj);
     if (bl.prefetch == 2 && t < 32) prefetch_bucket(rec, sstart, bstart, b + gridDim.x, t);
     __syncthreads();
     // hist[j] is now the end of key j: a leaf starts where its first key does
