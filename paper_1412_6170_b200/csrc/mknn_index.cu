@@ -149,6 +149,18 @@ __global__ void k_cell_info(const int32_t* __restrict__ z_map, const int32_t* __
             ((unsigned long long)sb << 38) | ((unsigned long long)leaf << 42);
 }
 
+// cell_info with the leaf ordinal replaced by the leaf's partition bucket:
+// the one-pass partition gets a point's bucket and key from one gather
+__global__ void k_cell_bucket(const unsigned long long* __restrict__ info,
+                              const uint16_t* __restrict__ leaf_bucket,
+                              const int32_t* __restrict__ scalars, int64_t ncap,
+                              unsigned long long* __restrict__ out) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ((int64_t)1 << (2 * scalars[0])) || c >= ncap) return;
+  const unsigned long long e = info[c];
+  out[c] = (e & ((1ull << 42) - 1)) | ((unsigned long long)leaf_bucket[e >> 42] << 42);
+}
+
 // Per point: the leaf (encode at l_deep -> z_map, quadindex.py:196-199;
 // engine.py:206) and the sub-cell key sub_base[leaf] + sub, where sub is the
 // point's Morton code s levels below the leaf's level.  The l_deep code is
@@ -604,7 +616,7 @@ __global__ void k_cap_plan(const uint32_t* __restrict__ prev, int32_t* __restric
 __global__ void __launch_bounds__(PT_THREADS) k_partition_keys(
     const long long* __restrict__ ids, const double* __restrict__ x, const double* __restrict__ y,
     int64_t n, Region r, const int32_t* __restrict__ scalars,
-    const unsigned long long* __restrict__ info, const uint16_t* __restrict__ leaf_bucket,
+    const unsigned long long* __restrict__ cell_bucket,
     const int32_t* __restrict__ sstart, int32_t* __restrict__ cursor, StoreRec* __restrict__ out,
     unsigned long long* clamped, unsigned long long* overflow, int64_t index_base = 0) {
   __shared__ int hist[PT_BUCKETS], gbase[PT_BUCKETS];
@@ -632,10 +644,10 @@ __global__ void __launch_bounds__(PT_THREADS) k_partition_keys(
     if (t + j * PT_THREADS < tile_n) {
       // geometry.py:215-220 count_outside
       outside_n += outside(rc[j].x, rc[j].y, r);
-      uint32_t leaf, key;
-      point_key(rc[j].x, rc[j].y, r, l_deep, info, leaf, key);
+      uint32_t bkt, key;
+      point_key(rc[j].x, rc[j].y, r, l_deep, cell_bucket, bkt, key);
       rc[j].key = key;
-      bk[j] = __ldg(&leaf_bucket[leaf]);
+      bk[j] = (int)bkt;
     }
   }
   __syncthreads();
@@ -1127,6 +1139,7 @@ int index_alloc(DevIndex& ix, int l_max, int th_quad) {
   MKNN_CUDA_OK(cudaMalloc(&ix.bkey, sizeof(int32_t) * (PT_BUCKETS + 1)));
   MKNN_CUDA_OK(cudaMalloc(&ix.leaf_first, sizeof(int32_t) * (PT_BUCKETS + 1)));
   MKNN_CUDA_OK(cudaMalloc(&ix.leaf_bucket, sizeof(uint16_t) * ncap));
+  MKNN_CUDA_OK(cudaMalloc(&ix.cell_bucket, sizeof(unsigned long long) * ncap));
   return 0;
 }
 
@@ -1148,6 +1161,7 @@ void index_free(DevIndex& ix) {
   cudaFree(ix.bkey);
   cudaFree(ix.leaf_first);
   cudaFree(ix.leaf_bucket);
+  cudaFree(ix.cell_bucket);
   ix = DevIndex{};
 }
 
@@ -1206,6 +1220,8 @@ int index_build(DevIndex& ix, const Region& r, const double* x, const double* y,
   MKNN_LAUNCH k_leaf_bucket<<<blocks_for(ncap + 1), TPB, 0, s>>>(pre, ix.leaf_sub_base, ix.scalars, ncap,
                                                                 ix.leaf_bucket, ix.bkey,
                                                                 ix.leaf_first);
+  MKNN_LAUNCH k_cell_bucket<<<blocks_for(ncap), TPB, 0, s>>>(ix.cell_info, ix.leaf_bucket, ix.scalars,
+                                                            ncap, ix.cell_bucket);
   MKNN_CUDA_OK(cudaMemsetAsync(ix.bload, 0, sizeof(uint32_t) * PT_BUCKETS, s));
   MKNN_LAUNCH k_bucket_load<<<blocks_for(ncap), TPB, 0, s>>>(ix.build_counts, ix.leaf_bucket,
                                                              ix.scalars, ncap, ix.bload);
@@ -1285,7 +1301,7 @@ int store_prepartition(DevStore& st, const DevIndex& ix, const Region& r, const 
   if (plan) MKNN_LAUNCH k_cap_plan<<<1, PT_BUCKETS, 0, s>>>(st.bcnt, st.sstart, st.cursor);
   if (hi > lo)
     MKNN_LAUNCH k_partition_keys<<<(unsigned)((hi - lo + PT_TILE - 1) / PT_TILE), PT_THREADS, 0, s>>>(
-        ids + lo, x + lo, y + lo, hi - lo, r, ix.scalars, ix.cell_info, ix.leaf_bucket, st.sstart,
+        ids + lo, x + lo, y + lo, hi - lo, r, ix.scalars, ix.cell_bucket, st.sstart,
         st.cursor, st.rec, pre, pre + 1, lo);
   MKNN_CUDA_OK(cudaGetLastError());
   return 0;
@@ -1330,7 +1346,7 @@ int store_index_objects(DevStore& st, const DevIndex& ix, const Region& r, const
       } else {
         MKNN_LAUNCH k_cap_plan<<<1, PT_BUCKETS, 0, s>>>(st.bcnt, st.sstart, st.cursor);
         MKNN_LAUNCH k_partition_keys<<<(unsigned)((n + PT_TILE - 1) / PT_TILE), PT_THREADS, 0, s>>>(
-            ids, x, y, n, r, ix.scalars, ix.cell_info, ix.leaf_bucket, st.sstart, st.cursor, st.rec,
+            ids, x, y, n, r, ix.scalars, ix.cell_bucket, st.sstart, st.cursor, st.rec,
             dev_clamped, dev_overflow);
       }
       MKNN_LAUNCH k_bucket_counts<<<1, PT_BUCKETS, 0, s>>>(st.sstart, st.cursor, st.bcnt, st.bstart);

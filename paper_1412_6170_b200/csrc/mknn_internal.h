@@ -70,6 +70,7 @@ struct DevIndex {
   int32_t* bkey = nullptr;       // leaf-aligned partition buckets: bucket b = keys [bkey[b], bkey[b+1])
   int32_t* leaf_first = nullptr;  // bucket b holds leaves [leaf_first[b], leaf_first[b+1])
   uint16_t* leaf_bucket = nullptr;  // bucket of every leaf
+  unsigned long long* cell_bucket = nullptr;  // cell_info with the leaf's bucket in bits 42-63
   int l_max = 0;
   int th_quad = 0;
 };
