@@ -46,6 +46,20 @@ namespace mknn {
 
 namespace {
 
+// k > 32: the running lists live only in shared memory (visit_leaf_sm);
+// -DMKNN_SMEM_LIST=0 restores register-resident lists (A/B)
+#ifndef MKNN_SMEM_LIST
+#define MKNN_SMEM_LIST 1
+#endif
+constexpr bool SMEM_LIST = MKNN_SMEM_LIST;
+// 32 < k <= 128 launch shape: warps per CTA, resident CTAs per SM
+#ifndef MKNN_K128_WARPS
+#define MKNN_K128_WARPS 16
+#endif
+#ifndef MKNN_K128_MINB
+#define MKNN_K128_MINB 1
+#endif
+
 template <int KPL>
 struct List {
   double d[KPL];
@@ -739,6 +753,149 @@ __device__ __forceinline__ void merge_buffer_k(List<KPL>& L, const double* bufd,
     L = merge_buffer<KPL>(L, bufd, bufi, nbuf, rowd, rowi, lane);
 }
 
+// ---- k > 32 with the list resident in shared memory ----------------------
+// The list's home (ld/li, N entries, element e at [e]) is the only copy: a
+// leaf visit holds just the k-th key in registers while it scans, and a
+// merge reads the list keys from the home, gathers the merged entries into
+// registers and writes them back.  The scan loop and the navigation then
+// carry no list registers (2 * KPL fp64/int64 pairs), which is what bounds
+// the resident warps of the k > 32 kernel.
+template <int KPL>
+__device__ __forceinline__ void list_load_sm(List<KPL>& L, const double* ld, const long long* li,
+                                             int lane) {
+#pragma unroll
+  for (int s = 0; s < KPL; s++) {
+    L.d[s] = ld[s * 32 + lane];
+    L.id[s] = li[s * 32 + lane];
+  }
+}
+template <int KPL>
+__device__ __forceinline__ void list_store_sm(const List<KPL>& L, double* ld, long long* li, int lane) {
+#pragma unroll
+  for (int s = 0; s < KPL; s++) {
+    ld[s * 32 + lane] = L.d[s];
+    li[s * 32 + lane] = L.id[s];
+  }
+}
+
+template <int KPL>
+__device__ __forceinline__ void kth_sm(const double* ld, const long long* li, int k, double& kd,
+                                       long long& ki) {
+  kd = ld[k - 1];
+  ki = li[k - 1];
+}
+
+template <int KPL>
+__device__ __forceinline__ void merge_sm(double* ld, long long* li, const double* bufd,
+                                         const long long* bufi, int nbuf, int lane) {
+  constexpr int N = 32 * KPL;
+  if constexpr (KPL > 4) {  // 64-bit key networks (merge_buffer re-homes the list itself)
+    List<KPL> L;
+    list_load_sm<KPL>(L, ld, li, lane);
+    L = merge_buffer<KPL>(L, bufd, bufi, nbuf, ld, li, lane);
+    list_store_sm<KPL>(L, ld, li, lane);
+    __syncwarp();
+    return;
+  } else {
+    constexpr int SB = KPL <= 2 ? 7 : 8;  // bits for 2N sources
+    uint32_t kb[KPL], m[KPL];
+#pragma unroll
+    for (int s = 0; s < KPL; s++) {
+      const int e = (s << 5) | lane;
+      kb[s] = e < nbuf ? akey(bufd[e], SB, (uint32_t)(N + e)) : (~0u << SB) | (uint32_t)(N + e);
+    }
+    sort_used_slots<KPL>(kb, nbuf, lane);
+    uint32_t kept_max = 0, drop_min = ~0u;
+#pragma unroll
+    for (int s = 0; s < KPL; s++) {
+      const int e = (s << 5) | lane;
+      const uint32_t kl = akey(ld[e], SB, (uint32_t)e);
+      const uint32_t rb = __shfl_sync(FULL, kb[KPL - 1 - s], 31 - lane);
+      m[s] = min(kl, rb);
+      kept_max = max(kept_max, m[s]);
+      drop_min = min(drop_min, max(kl, rb));
+    }
+    kept_max = __reduce_max_sync(FULL, kept_max);
+    drop_min = __reduce_min_sync(FULL, drop_min);
+    const bool cut_tie = ((kept_max ^ drop_min) >> SB) == 0 && (kept_max >> SB) < (AKEY_INF >> SB);
+#pragma unroll
+    for (int j = N >> 1; j > 0; j >>= 1) step_key<KPL>(m, lane, N, j);
+    const bool ties = akey32_ties<KPL>(m, SB, lane);
+    List<KPL> L;
+    if (cut_tie || (KPL < 4 && ties)) {  // exact (d2, id) networks
+      list_load_sm<KPL>(L, ld, li, lane);
+      L = merge_buffer_exact<KPL>(L, bufd, bufi, nbuf, lane);
+    } else {
+#pragma unroll
+      for (int s = 0; s < KPL; s++) {
+        const int src = (int)(m[s] & ((1u << SB) - 1u));
+        const bool from_list = src < N, pad = src - N >= nbuf;  // pad: an unused buffer slot
+        L.d[s] = from_list ? ld[src] : (pad ? DINF : bufd[src - N]);
+        L.id[s] = from_list ? li[src] : (pad ? IDMAX : bufi[src - N]);
+      }
+      if (KPL >= 4 && ties) repair_runs<KPL>(L, lane);
+    }
+    __syncwarp();
+    list_store_sm<KPL>(L, ld, li, lane);
+    __syncwarp();
+  }
+}
+
+template <int KPL>
+__device__ __forceinline__ void visit_leaf_sm(int k, int leaf, double qx, double qy, long long me,
+                                              const SearchArgs& a, int lane, double* bufd,
+                                              long long* bufi, double* ld, long long* li, bool own) {
+  constexpr int N = 32 * KPL;
+  const int ob = __ldg(&a.cell_start[leaf]), oe = __ldg(&a.cell_start[leaf + 1]);
+  const int c0 = __ldg(&a.chunk_start[leaf]), c1 = c0 + (oe - ob + chunk_for_k(32 * KPL) - 1) / chunk_for_k(32 * KPL);
+  const unsigned lt = (1u << lane) - 1u;
+  prof_add(a.prof, own ? PROF_OWN_CHUNKS_TOTAL : PROF_EXP_CHUNKS_TOTAL, c1 - c0, lane);
+  if (!own) prof_add(a.prof, PROF_EXP_LEAF_VISITS, 1, lane);
+  double kd;
+  long long ki;
+  kth_sm<KPL>(ld, li, k, kd, ki);
+  int nbuf = 0;
+  for (int g = c0; g < c1; g += 32) {
+    bool live = g + lane < c1;
+    double md = DINF;
+    if (live) md = mindist2_box(a.box[g + lane], qx, qy);
+    for (;;) {
+      const bool cand = live && md <= kd;
+      if (!__any_sync(FULL, cand)) break;
+      const unsigned key =
+          cand ? ((__float_as_uint(__double2float_rd(md)) & ~31u) | (unsigned)lane) : 0xffffffffu;
+      int cb;
+      bool v;
+      pick_chunks<chunk_for_k(32 * KPL)>(key, live, lane, ob, oe, g - c0, cb, v);
+      const StoreRec r = load_rec(a.obj, cb, v);
+      prof_add(a.prof, own ? PROF_OWN_CHUNKS_SCANNED : PROF_EXP_CHUNKS_SCANNED, 1, lane);
+      const double d2 = v ? pair_d2(qx, qy, r.x, r.y) : DINF;
+      const bool pass = v && d2 <= kd && r.id != me && key_less(d2, r.id, kd, ki);
+      const unsigned m = __ballot_sync(FULL, pass);
+      if (m) {
+        if (pass) {
+          const int pos = nbuf + __popc(m & lt);
+          bufd[pos] = d2;
+          bufi[pos] = r.id;
+        }
+        nbuf += __popc(m);
+        prof_add(a.prof, PROF_ADMITTED, __popc(m), lane);
+        __syncwarp();
+        if (nbuf > N - 32) {
+          prof_add(a.prof, PROF_SORT_MERGES, 1, lane);
+          merge_sm<KPL>(ld, li, bufd, bufi, nbuf, lane);
+          nbuf = 0;
+          kth_sm<KPL>(ld, li, k, kd, ki);
+        }
+      }
+    }
+  }
+  if (nbuf) {
+    prof_add(a.prof, PROF_INSERTS, 1, lane);
+    merge_sm<KPL>(ld, li, bufd, bufi, nbuf, lane);
+  }
+}
+
 template <int KPL>
 __device__ __forceinline__ void visit_leaf_buf(List<KPL>& L, int k, int leaf, double qx, double qy,
                                                long long me, const SearchArgs& a, int lane,
@@ -1044,6 +1201,22 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
       const double rr = sqrt(p_kd) + sqrt(dx * dx + dy * dy);
       cap = rr * rr * (1.0 + 0x1p-30) + 0x1p-1000;
     }
+    if constexpr (KPL > 1 && SMEM_LIST) {
+      double* ld = sd + j * N;
+      long long* li = si + j * N;
+#pragma unroll
+      for (int s = 0; s < KPL; s++) {
+        ld[s * 32 + lane] = DINF;
+        li[s * 32 + lane] = IDMAX;
+      }
+      __syncwarp();
+      visit_leaf_sm<KPL>(k, (int)jown, jx, jy, jme, a, lane, bufd, bufi, ld, li, true);
+      double kd;
+      long long ki;
+      kth_sm<KPL>(ld, li, k, kd, ki);
+      if (lane == j) thr = kd;
+      continue;
+    }
     List<KPL> L;
 #pragma unroll
     for (int s = 0; s < KPL; s++) {
@@ -1110,6 +1283,16 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
       const int jl = __shfl_sync(FULL, li, j);
       const double jx = __shfl_sync(FULL, qx, j), jy = __shfl_sync(FULL, qy, j);
       const long long jme = __shfl_sync(FULL, me, j);
+      if constexpr (KPL > 1 && SMEM_LIST) {
+        double* ld = sd + j * N;
+        long long* li = si + j * N;
+        visit_leaf_sm<KPL>(k, jl, jx, jy, jme, a, lane, bufd, bufi, ld, li, false);
+        double kd;
+        long long ki;
+        kth_sm<KPL>(ld, li, k, kd, ki);
+        if (lane == j) thr = kd;
+        continue;
+      }
       List<KPL> L;
       int64_t o = 0;
       if constexpr (ROWS) {
@@ -2094,7 +2277,7 @@ int search_launch(const SearchArgs& a, cudaStream_t s) {
   // 128 with 32-bit merge keys: 2 queries per warp 12.6 ms, 1: 13.5, 4:
   // 13.0, 8: 16.0)
   if (a.k <= 64) return launch_batched<2, 8, 4>(a, s);
-  if (a.k <= 128) return launch_batched<4, 2, 16>(a, s);
+  if (a.k <= 128) return launch_batched<4, 2, MKNN_K128_WARPS, MKNN_K128_MINB>(a, s);
   if (a.k <= 256) return launch_batched<8, 1, 8>(a, s);
   if (a.k <= 512) return launch_batched<16, 1, 4>(a, s);
   return fail_msg(E_UNSUPPORTED, "k > 512 is not supported by the device top-k");
