@@ -59,6 +59,9 @@ constexpr bool SMEM_LIST = MKNN_SMEM_LIST;
 #ifndef MKNN_K128_MINB
 #define MKNN_K128_MINB 1
 #endif
+#ifndef MKNN_K128_B
+#define MKNN_K128_B 2
+#endif
 
 template <int KPL>
 struct List {
@@ -2277,7 +2280,7 @@ int search_launch(const SearchArgs& a, cudaStream_t s) {
   // 128 with 32-bit merge keys: 2 queries per warp 12.6 ms, 1: 13.5, 4:
   // 13.0, 8: 16.0)
   if (a.k <= 64) return launch_batched<2, 8, 4>(a, s);
-  if (a.k <= 128) return launch_batched<4, 2, MKNN_K128_WARPS, MKNN_K128_MINB>(a, s);
+  if (a.k <= 128) return launch_batched<4, MKNN_K128_B, MKNN_K128_WARPS, MKNN_K128_MINB>(a, s);
   if (a.k <= 256) return launch_batched<8, 1, 8>(a, s);
   if (a.k <= 512) return launch_batched<16, 1, 4>(a, s);
   return fail_msg(E_UNSUPPORTED, "k > 512 is not supported by the device top-k");
