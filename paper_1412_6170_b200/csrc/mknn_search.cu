@@ -59,6 +59,13 @@ constexpr bool SMEM_LIST = MKNN_SMEM_LIST;
 #ifndef MKNN_K128_MINB
 #define MKNN_K128_MINB 1
 #endif
+// warps of at most two queries (k > 64) navigate each query with 16 / 32
+// lanes (navigate_grp) with -DMKNN_GROUP_NAV=1 (A/B: measured slower, the
+// prunes mostly happen at the first level of a chain)
+#ifndef MKNN_GROUP_NAV
+#define MKNN_GROUP_NAV 0
+#endif
+constexpr bool GROUP_NAV = MKNN_GROUP_NAV;
 #ifndef MKNN_K128_B
 #define MKNN_K128_B 2
 #endif
@@ -1066,6 +1073,100 @@ __device__ __forceinline__ int navigate(const SearchArgs& a, int l_deep, int dir
   }
 }
 
+// navigate for one query run by a group of G lanes (lane j of the group,
+// gmask = the group's lanes): the walk descends from the coarsest aligned
+// quadrant through the quadrants holding the cursor until one is pruned or
+// the leaf is reached, so lane j evaluates level lvl0 + j of that chain at
+// once and the first pruned level is the one the serial walk prunes at --
+// the same prune events, cursor moves and leaf as navigate, one parallel
+// step per prune or leaf resolution instead of one step per level.  Used
+// where a warp holds at most two queries (k > 64) and its other lanes
+// would idle through the serial walk.  Returns the leaf (every lane of the
+// group); prunes / viol are counted identically in every lane of the group.
+__device__ __forceinline__ int navigate_grp(const SearchArgs& a, int l_deep, int dir, int& cursor,
+                                            double thr, double qx, double qy, long long me,
+                                            uint32_t& prunes, uint32_t& viol,
+                                            const double2* __restrict__ cw, int j, unsigned gmask) {
+  const int n_codes = 1 << (2 * l_deep);
+  int pos = cursor;
+  if (dir ? pos >= n_codes : pos < 0) return -1;
+  const bool full = thr < DINF;  // engine.py:415
+  for (;;) {
+    const int lvl0 = full ? coarsest_level(pos, dir, l_deep) : l_deep;
+    const int lvl = lvl0 + j;
+    bool pr = false;
+    uint32_t qc = 0;
+    if (full && lvl <= l_deep) {
+      qc = (uint32_t)(pos >> (2 * (l_deep - lvl)));
+      double md2;
+      if (cw) {
+        const double2 wh = cw[lvl];
+        md2 = mindist2_cell_w(qc, wh.x, wh.y, a.r, qx, qy);
+      } else {
+        md2 = mindist2_cell(lvl, qc, a.r, qx, qy);
+      }
+      pr = md2 > thr;  // strict, as navigate
+    }
+    const unsigned pm = __ballot_sync(gmask, pr) & gmask;
+    if (pm) {  // prune at the first pruned level of the chain (engine.py:447-460)
+      const int p = (__ffs(pm) - 1) - (__ffs(gmask) - 1);
+      const int plvl = lvl0 + p;
+      prunes++;
+      if (a.audit) {
+        const bool v = j == p && audit_quadrant(a.z_map, a.cell_start, a.obj, a.r, l_deep, plvl,
+                                                qc, thr, qx, qy, me);
+        if (__ballot_sync(gmask, v) & gmask) viol++;
+      }
+      const int delta = l_deep - plvl;
+      pos += dir ? (1 << (2 * delta)) : -(1 << (2 * delta));
+    } else {  // every level of the chain passes: resolve the leaf (engine.py:467-487)
+      const int li = __ldg(&a.z_map[pos]);
+      const int key = (int)__ldg(&a.leaf_key[li]);
+      const int after = dir ? key + (int)__ldg(&a.leaf_span[li]) : key - 1;
+      if (__ldg(&a.cell_start[li + 1]) > __ldg(&a.cell_start[li])) {
+        cursor = after;
+        return li;
+      }
+      pos = after;  // empty leaf: skip it whole
+    }
+    if (dir ? pos >= n_codes : pos < 0) {  // exhausted (engine.py:489-494)
+      cursor = pos;
+      return -1;
+    }
+  }
+}
+
+// one navigate call for each of the warp's B <= 2 queries (owner lane q),
+// each run by its 32 / B lanes with navigate_grp; li / cur / prunes / viol
+// of an active owner lane updated as navigate would
+template <int B>
+__device__ __forceinline__ void nav_grouped(const SearchArgs& a, int l_deep, bool go_right, bool act,
+                                            int& cur, double thr, double qx, double qy, long long me,
+                                            uint32_t& prunes, uint32_t& viol,
+                                            const double2* __restrict__ cw, int lane, int& li) {
+  constexpr int G = 32 / B;
+  const int g = lane / G, j = lane % G;
+  const unsigned gmask = G == 32 ? FULL : (((1u << G) - 1u) << (g * G));
+  const int gr = __shfl_sync(FULL, (int)go_right, g);
+  const int ga = __shfl_sync(FULL, (int)act, g);
+  int gc = __shfl_sync(FULL, cur, g);
+  const double gt = __shfl_sync(FULL, thr, g);
+  const double gx = __shfl_sync(FULL, qx, g), gy = __shfl_sync(FULL, qy, g);
+  const long long gm = __shfl_sync(FULL, me, g);
+  uint32_t gp = 0, gv = 0;
+  int gl = -1;
+  if (ga) gl = navigate_grp(a, l_deep, gr, gc, gt, gx, gy, gm, gp, gv, cw, j, gmask);
+  const int src = (lane % B) * G;
+  const int rl = __shfl_sync(FULL, gl, src), rc = __shfl_sync(FULL, gc, src);
+  const uint32_t rp = __shfl_sync(FULL, gp, src), rv = __shfl_sync(FULL, gv, src);
+  if (act) {
+    li = rl;
+    cur = rc;
+    prunes += rp;
+    viol += rv;
+  }
+}
+
 // k <= 32 lists kept in the caller's output rows (k slots each, d2 until
 // the emit turns them into distances): no shared memory, so L1 keeps the
 // leaf records and chunk boxes
@@ -1261,9 +1362,13 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
     const bool act = act_l || act_r;
     next_right = !go_right;
     int li = -1;
-    if (act) {
-      int cur = go_right ? cur_r : cur_l;
+    int cur = go_right ? cur_r : cur_l;
+    if constexpr (GROUP_NAV && B <= 2 && !ROWS) {
+      nav_grouped<B>(a, l_deep, go_right, act, cur, thr, qx, qy, me, prunes, viol, cw, lane, li);
+    } else if (act) {
       li = navigate(a, l_deep, go_right ? 1 : 0, cur, thr, qx, qy, me, prunes, viol, cw);
+    }
+    if (act) {
       if (go_right) {
         calls_r++;
         cur_r = cur;

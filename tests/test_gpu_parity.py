@@ -663,3 +663,25 @@ def test_repeated_issuers_on_a_wider_id_range():
             res = eng.process_tick(ids, x, y, qi, x[sel], y[sel])
             assert_same(res, orc.brute_force_knn(ids, x, y, qi, x[sel], y[sel], 5))
             assert eng.last_metrics.tick == t
+
+
+@pytest.mark.parametrize("k", [100, 200, 512])
+def test_grouped_navigation_metrics_vs_port(k):
+    """k > 64 runs each query's navigate calls on a lane group (navigate_grp:
+    the levels of the descent chain evaluated at once).  Rows, prune events,
+    iterations and active counts equal the reference engine's serial walk
+    (engine.py:396-503), and the prune audit (engine.py:529-554) runs through
+    the grouped path without violations."""
+    from paper_1412_6170_b200.engine import resolve_th_quad
+    snap = synth.place(60_000, "gaussian", seed=21, hotspots=5, sigma=700.0)
+    qi, qx, qy = synth.queries(snap, 3000, seed=21)
+    th = resolve_th_quad("auto", k)
+    with Engine(EngineConfig(k=k, region=synth.REGION, audit_pruning=True)) as eng:
+        res = eng.process_tick(snap.ids, snap.x, snap.y, qi, qx, qy)
+        m = eng.last_metrics
+    want = orc.engine_tick(snap.ids, snap.x, snap.y, qi, qx, qy, k, synth.REGION, th)
+    assert_same(res, want)
+    for key in ("distance_evals", "pruned_leaves", "iterations_left", "iterations_right",
+                "active_left", "active_right"):
+        assert getattr(m, key) == want.metrics[key], (key, getattr(m, key), want.metrics[key])
+    assert m.pruned_leaves > 0 and m.pruning_violations == 0
