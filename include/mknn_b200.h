@@ -62,6 +62,9 @@ typedef struct mknn_metrics {
     int64_t t_build_us;
     int64_t t_index_objects_us;
     int64_t t_index_queries_us;
+    /* first_iteration and the direction loop run in one search kernel per
+       query batch: its CUDA-event time split by the batches' measured
+       (%globaltimer) warp time in the own-leaf pass */
     int64_t t_first_iteration_us;
     int64_t t_loop_us;
     int64_t t_total_us;

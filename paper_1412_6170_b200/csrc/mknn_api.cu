@@ -710,6 +710,7 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
       a.work = h->work;
       a.own_pos = h->own_pos;
       a.own_thr = h->own_thr;
+      a.phase_ns = h->counters + 6;  // zeroed with the counters each tick
       a.audit = h->cfg.audit_pruning;
       {
         static const char* dp = getenv("MKNN_DEBUG_PHASE");
@@ -950,8 +951,16 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
   m.t_build_us = us_between(h->ev[0], h->ev[1]);
   m.t_index_objects_us = us_between(h->ev[1], h->ev[2]);
   m.t_index_queries_us = us_between(h->ev[2], h->ev[3]);
-  m.t_first_iteration_us = 0;  // fused into the search kernel (t_loop_us)
-  m.t_loop_us = us_between(h->ev[3], h->ev[4]);
+  {
+    // the search kernel runs first_iteration and the direction loop per
+    // query batch: its event time is split by the batches' measured warp
+    // time in the own-leaf pass (engine.py:641-642's two phases)
+    const int64_t t_search = us_between(h->ev[3], h->ev[4]);
+    const double own = (double)cnt[6], all = (double)cnt[7];
+    m.t_first_iteration_us =
+        all > 0.0 ? std::min<int64_t>(t_search, (int64_t)(t_search * (own / all) + 0.5)) : 0;
+    m.t_loop_us = t_search - m.t_first_iteration_us;
+  }
   m.t_emit_us = us_between(h->ev[4], h->ev[5]);
 
   h->last_tick_ok = true;

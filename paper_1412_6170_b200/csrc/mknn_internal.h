@@ -284,6 +284,10 @@ struct SearchArgs {
   // k-th d2, by leaf-grouped position; [nq * 32] and [nq]
   int32_t* own_pos;
   double* own_thr;
+  // [2] warp-time (ns, %globaltimer) of the query batches spent in the
+  // own-leaf pass (first_iteration) and in the whole walk: the host splits
+  // the search kernel's time into t_first_iteration_us / t_loop_us by it
+  unsigned long long* phase_ns;
 };
 
 // T from task keys: sorts keys in place (alt buffer) and sums the leaf

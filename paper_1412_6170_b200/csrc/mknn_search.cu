@@ -287,6 +287,21 @@ __device__ __forceinline__ void prof_add(unsigned long long* prof, int i, unsign
   if (MKNN_PROFILE && prof && lane == 0 && v) atomicAdd(&prof[i], v);
 }
 
+// %globaltimer (ns) and the phase split of a query batch: first_iteration
+// (own leaf) and the whole walk, added by one lane (SearchArgs::phase_ns)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void phase_add(unsigned long long* ph, unsigned long long t0,
+                                          unsigned long long t1, unsigned long long t2) {
+  if (ph) {
+    atomicAdd(&ph[0], t1 - t0);
+    atomicAdd(&ph[1], t2 - t0);
+  }
+}
+
 // Admit the candidates of one lane-per-candidate batch into the list.
 // cand (cd, ci) is (+inf, IDMAX) on lanes that do not pass; m = ballot of
 // passing lanes.  Few survivors are inserted one by one with warp shuffles;
@@ -1295,6 +1310,8 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
   double p_kd = DINF, p_x = 0.0, p_y = 0.0;
   long long p_id = IDMAX;  // this lane's entry of the previous list
   uint32_t p_own = 0xffffffffu;
+  __shared__ unsigned long long ph_sh[WARPS][2];  // phase timestamps (lane 0; no registers held)
+  if (lane == 0) ph_sh[w][0] = gtimer();
   for (int j = 0; j < nb; j++) {
     const double jx = __shfl_sync(FULL, qx, j), jy = __shfl_sync(FULL, qy, j);
     const long long jme = __shfl_sync(FULL, me, j);
@@ -1349,6 +1366,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
     }
   }
   __syncwarp();
+  if (lane == 0) ph_sh[w][1] = gtimer();
 
   // direction loop, left first (engine.py:645-681)
   // per query: left, right, left, ... (engine.py:645-681); a drained
@@ -1425,6 +1443,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
     }
     __syncwarp();
   }
+  if (lane == 0) phase_add(a.phase_ns, ph_sh[w][0], ph_sh[w][1], gtimer());
 
   // _emit: canonical order already; sqrt correctly rounded (engine.py:706)
   if constexpr (ROWS && KPL == 1) {
@@ -1845,6 +1864,7 @@ __global__ void __launch_bounds__(32, MINB) k_search1(const __grid_constant__ Se
   static_assert(B <= 32, "one query per lane");
   __shared__ double2 cw_tab[MAX_L_MAX + 1];
   __shared__ int32_t lists[B * 32];  // the batch's lists as store positions
+  __shared__ unsigned long long ph_sh[2];  // phase timestamps (lane 0; no registers held)
   const int lane = threadIdx.x;
   const int l_deep = __ldg(&a.scalars[0]);
   if (lane <= l_deep)
@@ -1891,6 +1911,7 @@ __global__ void __launch_bounds__(32, MINB) k_search1(const __grid_constant__ Se
     // its list excludes this issuer (see k_search: d <= d_prev(k) + |q -
     // q_prev|, padded by 2^-30 relative; the list after the pass -- and the
     // navigation threshold taken from it, engine.py:415 -- is unchanged)
+    if (lane == 0) ph_sh[0] = gtimer();
     if constexpr (!FUSED) {
       for (int j = 0; j < nb; j++) lists[j * 32 + lane] = __ldg(&a.own_pos[(int64_t)(t0 + j) * 32 + lane]);
       if (mine) thr = __ldg(&a.own_thr[t0 + lane]);
@@ -1924,6 +1945,7 @@ __global__ void __launch_bounds__(32, MINB) k_search1(const __grid_constant__ Se
       excl = !__any_sync(FULL, L.id == nme);
       lists[j * 32 + lane] = lane < k ? L.pos : -1;
     }
+    if (lane == 0) ph_sh[1] = FUSED ? gtimer() : ph_sh[0];  // staged: k_own1 timed it
 
     // direction loop, left first (engine.py:645-681)
     // per query: left, right, left, ... (engine.py:645-681); a drained
@@ -1982,6 +2004,7 @@ __global__ void __launch_bounds__(32, MINB) k_search1(const __grid_constant__ Se
       }
       __syncwarp();
     }
+    if (lane == 0) phase_add(a.phase_ns, ph_sh[0], ph_sh[1], gtimer());
 
     // _emit: canonical order already; sqrt correctly rounded (engine.py:706);
     // every result row is written once (streaming stores)
@@ -2132,6 +2155,7 @@ __global__ void __launch_bounds__(32 * OWN_WARPS, OWN_CTAS_PER_SM) k_own1(const 
     mbar_wait(bar_a, phase & 1u);
     phase++;
 
+    const unsigned long long ph_t0 = gtimer();
     const int j0 = w * OWN_PER_WARP, j1 = min(j0 + OWN_PER_WARP, nb);
     double p_kd = DINF, p_x = 0.0, p_y = 0.0;
     uint32_t p_own = 0xffffffffu;
@@ -2167,6 +2191,10 @@ __global__ void __launch_bounds__(32 * OWN_WARPS, OWN_CTAS_PER_SM) k_own1(const 
       excl = j + 1 < j1 ? !__any_sync(FULL, L.id == sme[j + 1]) : false;
       a.own_pos[(t0 + j) * 32 + lane] = lane < k ? L.pos : -1;
       if (lane == 0) a.own_thr[t0 + j] = kd;
+    }
+    if (lane == 0) {
+      const unsigned long long te = gtimer();
+      phase_add(a.phase_ns, ph_t0, te, te);
     }
     __syncthreads();
   }

@@ -685,3 +685,18 @@ def test_grouped_navigation_metrics_vs_port(k):
                 "active_left", "active_right"):
         assert getattr(m, key) == want.metrics[key], (key, getattr(m, key), want.metrics[key])
     assert m.pruned_leaves > 0 and m.pruning_violations == 0
+
+
+@pytest.mark.parametrize("k", [8, 32, 128])
+def test_phase_split_first_iteration(k):
+    """engine.py:641-642 reports first_iteration and the direction loop as two
+    phases; the device runs both in one kernel per query batch and splits the
+    kernel's event time by the batches' measured own-leaf warp time."""
+    snap = synth.place(200_000, "uniform", seed=5)
+    qi, qx, qy = synth.queries(snap, 50_000, seed=5)
+    with Engine(EngineConfig(k=k, region=synth.REGION)) as eng:
+        for _ in range(2):
+            eng.process_tick(snap.ids, snap.x, snap.y, qi, qx, qy)
+            m = eng.last_metrics
+            assert m.t_first_iteration_us > 0 and m.t_loop_us >= 0
+            assert m.t_first_iteration_us + m.t_loop_us < m.t_total_us

@@ -19,4 +19,4 @@ with Engine(EngineConfig(k=32, region=synth.REGION)) as eng:
         eng.update(*ups[i % 4])
         out = eng.query_device(*dq, out=out)
         torch.cuda.synchronize(); dt = time.perf_counter() - t
-        if i % 5 == 4: print(i, round(dt * 1e6), eng.graph_stats, eng.last_metrics.t_index_objects_us, eng.last_metrics.t_loop_us)
+        if i % 5 == 4: print(i, round(dt * 1e6), eng.graph_stats, eng.last_metrics.t_index_objects_us, (eng.last_metrics.t_first_iteration_us + eng.last_metrics.t_loop_us))

@@ -26,7 +26,7 @@ with Engine(EngineConfig(k=k, region=synth.REGION)) as eng:
         dt = time.perf_counter() - t
         m = eng.last_metrics
         print(f"it {it}: wall {dt*1e3:.2f} ms build {m.t_build_us} idxobj {m.t_index_objects_us} "
-              f"idxq {m.t_index_queries_us} search {m.t_loop_us} emit {m.t_emit_us} us; "
+              f"idxq {m.t_index_queries_us} search {(m.t_first_iteration_us + m.t_loop_us)} emit {m.t_emit_us} us; "
               f"evals/q {m.distance_evals/nq:.1f} prunes/q {m.pruned_leaves/nq:.1f} "
               f"iters {m.iterations_left}/{m.iterations_right} rebuild {m.rebuild_flag}", flush=True)
     ix = eng.index
