@@ -1,4 +1,4 @@
-"""Small ticks for compute-sanitizer (dev tool): full, delta, sliced-host, k>32."""
+"""Small ticks for compute-sanitizer (dev tool): full, delta, sliced-host, k>32 (32-bit and 64-bit merge keys)."""
 import sys
 import numpy as np
 sys.path.insert(0, ".")
@@ -7,7 +7,7 @@ from paper_1412_6170_b200 import Engine, EngineConfig, Rect, synth
 rng = np.random.default_rng(1)
 snap = synth.place(20_000, "gaussian", seed=2, hotspots=3)
 qi, qx, qy = synth.queries(snap, 3_000, seed=2)
-for k in (8, 32, 100):
+for k in (8, 32, 100, 300):
     with Engine(EngineConfig(k=k, region=synth.REGION)) as e:
         r = e.process_tick(snap.ids, snap.x, snap.y, qi, qx, qy)
         e.load(snap.ids, snap.x, snap.y)
