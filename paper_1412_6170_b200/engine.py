@@ -141,6 +141,38 @@ def _tptr(t) -> int:
     return t.data_ptr() if t is not None and t.numel() else 0
 
 
+def _dev(t, dtype, name: str):
+    """A device input as a torch CUDA tensor: torch tensors as they are,
+    any other DLPack producer (CuPy, JAX, numba, ...) zero-copy through
+    torch.from_dlpack; the dtype and layout the C-ABI reads are checked."""
+    import torch
+
+    if not isinstance(t, torch.Tensor):
+        if not hasattr(t, "__dlpack__"):
+            raise TypeError(f"{name}: expected a CUDA tensor or a DLPack device array")
+        t = torch.from_dlpack(t)
+    if not t.is_cuda or t.dtype != dtype or not t.is_contiguous() or t.dim() != 1:
+        raise TypeError(f"{name}: expected a contiguous 1-D CUDA {dtype} array, "
+                        f"got {t.dtype} {tuple(t.shape)} on {t.device}")
+    return t
+
+
+def _on_cuda(a) -> bool:
+    """A CUDA device array (torch, or a DLPack producer on kDLCUDA /
+    kDLCUDAManaged)?"""
+    if hasattr(a, "is_cuda"):
+        return bool(a.is_cuda)
+    dd = getattr(a, "__dlpack_device__", None)
+    return dd is not None and int(dd()[0]) in (2, 13)
+
+
+def _dev_xy(ids, x, y):
+    import torch
+
+    return (_dev(ids, torch.int64, "ids"), _dev(x, torch.float64, "x"),
+            _dev(y, torch.float64, "y"))
+
+
 _CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the legacy NULL stream as a handle
 
 _POOL = None
@@ -411,8 +443,13 @@ class Engine:
     def tick_device(self, ids, x, y, q_issuer, qx, qy, out=None):
         """process_tick on torch CUDA tensors; returns a dict of device
         tensors (query_ids, lengths, offsets, neighbour_ids, distances) whose
-        CSR arrays are padded to nq*k (first n_results entries valid)."""
+        CSR arrays are padded to nq*k (first n_results entries valid).
+        Inputs may be any DLPack device arrays; the results are torch
+        tensors, themselves DLPack producers (``x.__dlpack__()``), so other
+        frameworks take them zero-copy."""
         h = self._handle()
+        ids, x, y = _dev_xy(ids, x, y)
+        q_issuer, qx, qy = _dev_xy(q_issuer, qx, qy)
         self._follow_torch_stream(q_issuer)
         nq = int(q_issuer.numel())
         out = out or self.alloc_device_out(nq, q_issuer.device)
@@ -451,7 +488,8 @@ class Engine:
         everything else carries forward (datasets.py:109-164).  Accepts host
         arrays or torch CUDA tensors."""
         h = self._handle()
-        if hasattr(ids, "is_cuda") and ids.is_cuda:
+        if _on_cuda(ids):
+            ids, x, y = _dev_xy(ids, x, y)
             self._follow_torch_stream(ids)
             N.check(N.lib().mknn_update_device(h, int(ids.numel()), _tptr(ids), _tptr(x), _tptr(y)),
                     h, "mknn_update_device")
@@ -485,7 +523,10 @@ class Engine:
         return self._result(qids, lens, nids, dist, m.n_results, offs)
 
     def query_device(self, q_issuer, qx, qy, out=None):
+        """query on device arrays (torch or any DLPack producer); returns the
+        device result dict of tick_device."""
         h = self._handle()
+        q_issuer, qx, qy = _dev_xy(q_issuer, qx, qy)
         self._follow_torch_stream(q_issuer)
         nq = int(q_issuer.numel())
         out = out or self.alloc_device_out(nq, q_issuer.device)

@@ -700,3 +700,42 @@ def test_phase_split_first_iteration(k):
             m = eng.last_metrics
             assert m.t_first_iteration_us > 0 and m.t_loop_us >= 0
             assert m.t_first_iteration_us + m.t_loop_us < m.t_total_us
+
+
+class _DLPackOnly:
+    """A device array seen only through the DLPack protocol (as CuPy / JAX
+    arrays are)."""
+
+    def __init__(self, t):
+        self._t = t
+
+    def __dlpack__(self, *args, **kw):
+        return self._t.__dlpack__(*args, **kw)
+
+    def __dlpack_device__(self):
+        return self._t.__dlpack_device__()
+
+
+def test_device_paths_take_and_give_dlpack():
+    """device-resident inputs and results through DLPack --
+    any DLPack producer is taken zero-copy, the results are DLPack producers,
+    and a wrong dtype fails loudly instead of being read as raw bytes."""
+    snap = synth.place(30_000, "uniform", seed=8)
+    qi, qx, qy = synth.queries(snap, 3_000, seed=8)
+    d = [torch.as_tensor(np.ascontiguousarray(a), device="cuda:0")
+         for a in (snap.ids, snap.x, snap.y, qi, qx, qy)]
+    with Engine(EngineConfig(k=16, region=synth.REGION)) as eng:
+        want = {k: v.clone() if hasattr(v, "clone") else v for k, v in eng.tick_device(*d).items()}
+        got = eng.tick_device(*[_DLPackOnly(t) for t in d])
+        for key in ("query_ids", "lengths", "offsets", "neighbour_ids", "distances"):
+            view = torch.from_dlpack(got[key].__dlpack__())
+            assert view.data_ptr() == got[key].data_ptr()
+            assert torch.equal(view, want[key]), key
+        eng.load(snap.ids, snap.x, snap.y)
+        upd = synth.updates(snap, 0.1, 0, seed=8)
+        eng.update(*[_DLPackOnly(torch.as_tensor(np.ascontiguousarray(a), device="cuda:0"))
+                     for a in upd])
+        q = eng.query_device(*[_DLPackOnly(t) for t in d[3:]])
+        assert q["n_results"] == 3_000 * 16
+        with pytest.raises(TypeError):
+            eng.tick_device(d[0].to(torch.int32), *d[1:])
