@@ -810,10 +810,75 @@ __device__ __forceinline__ void kth_sm(const double* ld, const long long* li, in
   ki = li[k - 1];
 }
 
+// a short buffer (nbuf <= RANK_MERGE_MAX) merged by ranks instead of
+// networks: candidate c goes to (# list entries < c) + (# candidates < c),
+// list entry e to e + (# candidates below it); exact (d2, id) compares,
+// keys are distinct (a candidate is never already listed), entries pushed
+// past N fall off.  k > 64 (lists of >= 4 slots): every partial flush
+// (nbuf <= 32, one candidate per lane) takes it -- k = 128 / 256: 11.85 ->
+// 11.21 / 53.97 -> 49.35 ms; at k <= 64 and with smaller thresholds it
+// measured neutral or slower (repo:profiles/r2_ab_rank_merge.txt).
+// -DMKNN_RANK_MERGE=T: threshold T <= 32 (A/B; 0 = off).
+#ifndef MKNN_RANK_MERGE
+#define MKNN_RANK_MERGE 32
+#endif
+constexpr int RANK_MERGE_MAX = MKNN_RANK_MERGE;
+
+template <int KPL>
+__device__ __forceinline__ void merge_rank_sm(double* ld, long long* li, const double* bufd,
+                                              const long long* bufi, int nbuf, int lane) {
+  constexpr int N = 32 * KPL;
+  const bool has = lane < nbuf;
+  const double cd = has ? bufd[lane] : DINF;
+  const long long ci = has ? bufi[lane] : IDMAX;
+  int rl = 0;  // list entries below the candidate (power-of-two lower bound)
+#pragma unroll
+  for (int step = N / 2; step > 0; step >>= 1)
+    if (key_less(ld[rl + step], li[rl + step], cd, ci)) rl += step;
+  if (key_less(ld[rl], li[rl], cd, ci)) rl++;
+  int rc = 0, sh[KPL];
+#pragma unroll
+  for (int s = 0; s < KPL; s++) sh[s] = 0;
+  for (int j = 0; j < nbuf; j++) {
+    const double dj = __shfl_sync(FULL, cd, j);
+    const long long ij = __shfl_sync(FULL, ci, j);
+    const int rj = __shfl_sync(FULL, rl, j);
+    rc += key_less(dj, ij, cd, ci) ? 1 : 0;
+#pragma unroll
+    for (int s = 0; s < KPL; s++) sh[s] += rj <= ((s << 5) | lane) ? 1 : 0;
+  }
+  double od[KPL];
+  long long oi[KPL];
+#pragma unroll
+  for (int s = 0; s < KPL; s++) {
+    od[s] = ld[(s << 5) | lane];
+    oi[s] = li[(s << 5) | lane];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int s = 0; s < KPL; s++) {
+    const int np = ((s << 5) | lane) + sh[s];
+    if (np < N) {
+      ld[np] = od[s];
+      li[np] = oi[s];
+    }
+  }
+  if (has && rl + rc < N) {
+    ld[rl + rc] = cd;
+    li[rl + rc] = ci;
+  }
+  __syncwarp();
+}
+
 template <int KPL>
 __device__ __forceinline__ void merge_sm(double* ld, long long* li, const double* bufd,
                                          const long long* bufi, int nbuf, int lane) {
   constexpr int N = 32 * KPL;
+  static_assert(RANK_MERGE_MAX <= 32, "one buffered candidate per lane");
+  if (KPL >= 4 && RANK_MERGE_MAX > 0 && nbuf <= RANK_MERGE_MAX) {
+    merge_rank_sm<KPL>(ld, li, bufd, bufi, nbuf, lane);
+    return;
+  }
   if constexpr (KPL > 4) {  // 64-bit key networks (merge_buffer re-homes the list itself)
     List<KPL> L;
     list_load_sm<KPL>(L, ld, li, lane);
