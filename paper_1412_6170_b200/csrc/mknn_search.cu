@@ -819,6 +819,14 @@ __device__ __forceinline__ void kth_sm(const double* ld, const long long* li, in
 // 11.21 / 53.97 -> 49.35 ms; at k <= 64 and with smaller thresholds it
 // measured neutral or slower (repo:profiles/r2_ab_rank_merge.txt).
 // -DMKNN_RANK_MERGE=T: threshold T <= 32 (A/B; 0 = off).
+// k > 32: the own-leaf cap from the previous query's list (k_search's
+// triangle-inequality bound) with -DMKNN_KCAP=1 (A/B: measured slower, the
+// buffered admission takes the first chunks whole either way)
+#ifndef MKNN_KCAP
+#define MKNN_KCAP 0
+#endif
+constexpr bool KCAP = MKNN_KCAP;
+
 #ifndef MKNN_RANK_MERGE
 #define MKNN_RANK_MERGE 32
 #endif
@@ -934,7 +942,8 @@ __device__ __forceinline__ void merge_sm(double* ld, long long* li, const double
 template <int KPL>
 __device__ __forceinline__ void visit_leaf_sm(int k, int leaf, double qx, double qy, long long me,
                                               const SearchArgs& a, int lane, double* bufd,
-                                              long long* bufi, double* ld, long long* li, bool own) {
+                                              long long* bufi, double* ld, long long* li, bool own,
+                                              double cap = DINF) {
   constexpr int N = 32 * KPL;
   const int ob = __ldg(&a.cell_start[leaf]), oe = __ldg(&a.cell_start[leaf + 1]);
   const int c0 = __ldg(&a.chunk_start[leaf]), c1 = c0 + (oe - ob + chunk_for_k(32 * KPL) - 1) / chunk_for_k(32 * KPL);
@@ -944,6 +953,10 @@ __device__ __forceinline__ void visit_leaf_sm(int k, int leaf, double qx, double
   double kd;
   long long ki;
   kth_sm<KPL>(ld, li, k, kd, ki);
+  if (cap < kd) {  // an upper bound of the own-leaf k-th (see k_search)
+    kd = cap;
+    ki = IDMAX;
+  }
   int nbuf = 0;
   for (int g = c0; g < c1; g += 32) {
     bool live = g + lane < c1;
@@ -976,6 +989,10 @@ __device__ __forceinline__ void visit_leaf_sm(int k, int leaf, double qx, double
           merge_sm<KPL>(ld, li, bufd, bufi, nbuf, lane);
           nbuf = 0;
           kth_sm<KPL>(ld, li, k, kd, ki);
+          if (cap < kd) {
+            kd = cap;
+            ki = IDMAX;
+          }
         }
       }
     }
@@ -1390,17 +1407,35 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_search(const SearchArgs a)
     if constexpr (KPL > 1 && SMEM_LIST) {
       double* ld = sd + j * N;
       long long* li = si + j * N;
+      // the previous query's own-pass list as a cap, as for k <= 32 above
+      // (all its k entries must exclude this issuer)
+      double capm = DINF;
+      if (KCAP && jown == p_own && p_kd < DINF) {
+        const long long* pli = si + (j - 1) * N;
+        bool hit = false;
+#pragma unroll
+        for (int s = 0; s < KPL; s++) hit |= pli[s * 32 + lane] == jme;
+        if (!__any_sync(FULL, hit)) {
+          const double dx = jx - p_x, dy = jy - p_y;
+          const double rr = sqrt(p_kd) + sqrt(dx * dx + dy * dy);
+          capm = rr * rr * (1.0 + 0x1p-30) + 0x1p-1000;
+        }
+      }
 #pragma unroll
       for (int s = 0; s < KPL; s++) {
         ld[s * 32 + lane] = DINF;
         li[s * 32 + lane] = IDMAX;
       }
       __syncwarp();
-      visit_leaf_sm<KPL>(k, (int)jown, jx, jy, jme, a, lane, bufd, bufi, ld, li, true);
+      visit_leaf_sm<KPL>(k, (int)jown, jx, jy, jme, a, lane, bufd, bufi, ld, li, true, capm);
       double kd;
       long long ki;
       kth_sm<KPL>(ld, li, k, kd, ki);
       if (lane == j) thr = kd;
+      p_kd = kd;
+      p_x = jx;
+      p_y = jy;
+      p_own = jown;
       continue;
     }
     List<KPL> L;
