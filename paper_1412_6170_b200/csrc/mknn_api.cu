@@ -279,6 +279,8 @@ struct mknn_engine {
   long long* out_qids = nullptr; int64_t cap_oq = 0;
   QueryStats* stats = nullptr; int64_t cap_stats = 0;
   int32_t* own_pos = nullptr; double* own_thr = nullptr; int64_t cap_own = 0;  // k_own1 -> k_search1
+  uint32_t* batch_order = nullptr; int64_t cap_bo = 0;  // k_search1's batch schedule
+  uint32_t* lpt_cnt = nullptr;
   unsigned long long* prof = nullptr;  // MKNN_PROF=1 work counters
   unsigned* work = nullptr;  // k_search1 batch counter
   unsigned long long* counters = nullptr;  // [0] evals [1] prunes [2] viol [3] clamped
@@ -400,6 +402,7 @@ int alloc_store(mknn_engine* h, int64_t n) {
     h->hist_cap = (int)(ncap + 2);
     MKNN_CUDA_OK(cudaMalloc(&h->hist, sizeof(uint32_t) * 2 * h->hist_cap));
     MKNN_CUDA_OK(cudaMalloc(&h->work, sizeof(unsigned) * 4));
+    MKNN_CUDA_OK(cudaMalloc(&h->lpt_cnt, sizeof(uint32_t) * 32));
   }
   if (n > h->st.cap) {
     int64_t nc = std::max<int64_t>(n, h->st.cap * 3 / 2);
@@ -484,7 +487,8 @@ std::vector<void*> engine_buffers(mknn_engine* h) {
           h->up_ids, h->up_x, h->up_y, h->tk, h->tk_alt, h->tk_cnt, h->tv, h->tv_alt, h->prof,
           h->mark, h->moved, h->d_nmoved, h->clamped_total, h->work, h->st.kstart_alt,
           h->st.fill, h->st.qcnt, h->st.qkstart, h->st.rmflag, h->st.rm_before, h->st.mkey,
-          h->own_pos, h->own_thr, h->st.slot_pos, h->st.deferred, h->st.n_deferred, h->st.bkt};
+          h->own_pos, h->own_thr, h->st.slot_pos, h->st.deferred, h->st.n_deferred, h->st.bkt,
+          h->batch_order, h->lpt_cnt};
 }
 
 // A tick whose enqueue sequence is a pure function of the key below can run
@@ -548,6 +552,9 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
     c = h->cap_own * 32;
     if ((rc = grow(h->own_pos, c, nq * 32))) return h->set_err(rc);
     h->cap_own = c / 32;
+  }
+  if (k > 16 && k <= 32 && nq > h->cap_bo) {  // batches of >= 4 queries: nq / 4 + 1 suffice
+    if ((rc = grow(h->batch_order, h->cap_bo, nq))) return h->set_err(rc);
   }
   const int64_t rows = std::max<int64_t>(nq * (int64_t)k, 1);
   if (rows > h->cap_rows) {
@@ -710,6 +717,8 @@ int core_tick_once(mknn_engine* h, int64_t n, const long long* ids, const double
       a.work = h->work;
       a.own_pos = h->own_pos;
       a.own_thr = h->own_thr;
+      a.batch_order = h->batch_order;
+      a.lpt_cnt = h->lpt_cnt;
       a.phase_ns = h->counters + 6;  // zeroed with the counters each tick
       a.audit = h->cfg.audit_pruning;
       {

@@ -279,6 +279,10 @@ struct SearchArgs {
   // k_search1: persistent CTAs take query batches from *work (zeroed by
   // search_launch before each launch)
   unsigned* work;
+  // k_search1: the order its work counter hands out the query batches
+  // (costliest own leaves first, see lpt_order); nullptr: batch order
+  uint32_t* batch_order;
+  uint32_t* lpt_cnt;  // [32] class counts and cursors of lpt_order
   // 16 < k <= 32: the own-leaf pass (k_own1) hands each query's list to the
   // expansion kernel (k_search1) as k store positions (32 slots) and its
   // k-th d2, by leaf-grouped position; [nq * 32] and [nq]

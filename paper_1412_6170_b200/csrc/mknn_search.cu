@@ -1980,6 +1980,7 @@ __global__ void __launch_bounds__(32, MINB) k_search1(const __grid_constant__ Se
     if (lane == 0) batch = atomicAdd(a.work, 1u);
     batch = __shfl_sync(FULL, batch, 0);
     if ((int64_t)batch * B >= a.nq) break;
+    if (a.batch_order) batch = __ldg(&a.batch_order[batch]);
     const int t0 = (int)batch * B;  // queries < 2^31 (uint32 orders)
     const int nb = (int)((a.nq - t0) < B ? (a.nq - t0) : B);
 
@@ -2392,6 +2393,59 @@ __global__ void k_rows_compact(const int32_t* __restrict__ len, const long long*
 
 }  // namespace
 
+// ---- batch scheduling for the persistent k_search1 --------------------
+// The work counter hands out batches in leaf-grouped order, so the last
+// batches handed out are as costly as any and the kernel ends on a tail of
+// partly idle SMs.  lpt_order hands them out costliest first (longest
+// processing time first, by the population of the batch's first own leaf
+// in 16 log2 classes), so the tail is made of the cheapest batches.  Order
+// only: every batch still runs whole, results are unchanged.  Within a
+// class the batches keep runs of up to 32 consecutive ones (warp-
+// aggregated cursors), so concurrently running warps still share leaves.
+// Off by default (MKNN_LPT=1 enables it): measured slower (tuning log).
+constexpr int LPT_CLASSES = 16;
+
+__device__ __forceinline__ int lpt_class(const SearchArgs& a, int64_t b, int B) {
+  const uint32_t q = __ldg(&a.q_order[b * B]);
+  const uint32_t leaf = __ldg(&a.q_leaf[q]);
+  const int pop = __ldg(&a.cell_start[leaf + 1]) - __ldg(&a.cell_start[leaf]);
+  return LPT_CLASSES - 1 - min(LPT_CLASSES - 1, 31 - __clz(max(pop, 1)));
+}
+
+__global__ void k_lpt_count(const __grid_constant__ SearchArgs a, int B, int64_t nbt) {
+  __shared__ uint32_t h[LPT_CLASSES];
+  if (threadIdx.x < LPT_CLASSES) h[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nbt;
+       b += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&h[lpt_class(a, b, B)], 1u);
+  __syncthreads();
+  if (threadIdx.x < LPT_CLASSES && h[threadIdx.x]) atomicAdd(&a.lpt_cnt[threadIdx.x], h[threadIdx.x]);
+}
+
+__global__ void k_lpt_place(const __grid_constant__ SearchArgs a, int B, int64_t nbt) {
+  __shared__ uint32_t base[LPT_CLASSES];
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < LPT_CLASSES) {
+    uint32_t x = 0;
+    for (int c = 0; c < (int)threadIdx.x; c++) x += a.lpt_cnt[c];
+    base[threadIdx.x] = x;
+  }
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); b0 < nbt; b0 += stride) {
+    const int64_t b = b0 + lane;
+    const int c = b < nbt ? lpt_class(a, b, B) : LPT_CLASSES;
+    const unsigned m = __match_any_sync(FULL, c);
+    const int leader = __ffs(m) - 1;
+    uint32_t off = 0;
+    if (lane == leader && c < LPT_CLASSES) off = atomicAdd(&a.lpt_cnt[LPT_CLASSES + c], (uint32_t)__popc(m));
+    off = __shfl_sync(FULL, off, leader);
+    if (c < LPT_CLASSES)
+      a.batch_order[base[c] + off + __popc(m & ((1u << lane) - 1u))] = (uint32_t)b;
+  }
+}
+
 template <int KPL, int B, int WARPS, int MINB = 1, bool ROWS = false>
 int launch_batched(const SearchArgs& a, cudaStream_t s) {
   constexpr int N = 32 * KPL;
@@ -2431,7 +2485,24 @@ int launch_search1(const SearchArgs& a, cudaStream_t s) {
   }
   const int64_t batches = (a.nq + B - 1) / B;
   int64_t grid = std::min<int64_t>(batches, (int64_t)sms * SEARCH1_CTAS_PER_SM);
-  MKNN_LAUNCH k_search1<B, SEARCH1_CTAS_PER_SM, FUSED><<<(unsigned)grid, 32, 0, s>>>(a);
+  // MKNN_LPT=1: costliest batches first (A/B; measured 2.6 % slower at cfg3:
+  // the tail is short and the leaf-grouped order's L2 sharing is worth more)
+  static const bool lpt = [] {
+    const char* e = getenv("MKNN_LPT");
+    return e && e[0] == '1';
+  }();
+  SearchArgs b = a;
+  if (!lpt || !a.batch_order || !a.lpt_cnt || batches < 2 * grid) {
+    b.batch_order = nullptr;
+  } else {
+    MKNN_CUDA_OK(cudaMemsetAsync(a.lpt_cnt, 0, 2 * LPT_CLASSES * sizeof(uint32_t), s));
+    const unsigned lg = (unsigned)std::min<int64_t>((batches + 255) / 256, (int64_t)sms * 2);
+    MKNN_LAUNCH k_lpt_count<<<lg, 256, 0, s>>>(a, B, batches);
+    MKNN_CUDA_OK(cudaGetLastError());
+    MKNN_LAUNCH k_lpt_place<<<lg, 256, 0, s>>>(a, B, batches);
+    MKNN_CUDA_OK(cudaGetLastError());
+  }
+  MKNN_LAUNCH k_search1<B, SEARCH1_CTAS_PER_SM, FUSED><<<(unsigned)grid, 32, 0, s>>>(b);
   MKNN_CUDA_OK(cudaGetLastError());
   return 0;
 }
