@@ -118,7 +118,7 @@ __global__ void k_fill_slots(HashSlot* ht, int64_t n) {
 }
 
 __global__ void k_hash_load(const long long* __restrict__ ids, int64_t n, HashSlot* ht,
-                            uint64_t mask, int32_t* winner) {
+                            uint64_t mask) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     // duplicate ids inside a snapshot: the first slot keeps the mapping
@@ -126,21 +126,24 @@ __global__ void k_hash_load(const long long* __restrict__ ids, int64_t n, HashSl
   }
 }
 
-// last update per id wins (datasets.py:130-131): winner[slot] = max index
+// last update per id wins (datasets.py:130-131): winner[slot] = max of
+// (batch sequence << 32 | index) -- a later batch's claims are larger than
+// any left by an earlier one, so the array is never reset between batches
 __global__ void k_update_claim(const long long* __restrict__ ids, int64_t nu, HashSlot* ht,
-                               uint64_t mask, int32_t* n_snap, int32_t* winner,
-                               int32_t* slot_of) {
+                               uint64_t mask, int32_t* n_snap, unsigned long long* winner,
+                               int32_t* slot_of, unsigned long long seq) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nu;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t s = hash_find_or_insert(ht, mask, ids[i], n_snap, true, -1);
     slot_of[i] = s;
-    atomicMax(&winner[s], (int32_t)i);
+    atomicMax(&winner[s], (seq << 32) | (unsigned long long)i);
   }
 }
 
 __global__ void k_update_apply(const long long* __restrict__ ids, const double* __restrict__ x,
                                const double* __restrict__ y, int64_t nu,
-                               const int32_t* __restrict__ slot_of, int32_t* winner,
+                               const int32_t* __restrict__ slot_of,
+                               const unsigned long long* __restrict__ winner, unsigned long long seq,
                                long long* sids, double* sx, double* sy, int32_t* mark,
                                int32_t epoch, int32_t* moved, int32_t* n_moved, bool track,
                                const int32_t* __restrict__ n_before) {
@@ -150,7 +153,7 @@ __global__ void k_update_apply(const long long* __restrict__ ids, const double* 
        i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t s = slot_of[i];
     bool first = false;
-    if (winner[s] == (int32_t)i) {
+    if (winner[s] == ((seq << 32) | (unsigned long long)i)) {
       if (s >= nb) sids[s] = ids[i];
       sx[s] = x[i];
       sy[s] = y[i];
@@ -172,11 +175,6 @@ __global__ void k_update_apply(const long long* __restrict__ ids, const double* 
   }
 }
 
-__global__ void k_update_reset(int64_t nu, const int32_t* __restrict__ slot_of, int32_t* winner) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nu;
-       i += (int64_t)gridDim.x * blockDim.x)
-    winner[slot_of[i]] = -1;
-}
 
 inline unsigned gs_blocks(int64_t n) {
   return (unsigned)std::min<int64_t>(std::max<int64_t>((n + 255) / 256, 1), 148 * 256);
@@ -296,7 +294,8 @@ struct mknn_engine {
   long long* snap_ids = nullptr; double *snap_x = nullptr, *snap_y = nullptr; int64_t cap_snap = 0;
   int64_t n_snap = 0;
   HashSlot* ht = nullptr; int64_t hcap = 0;  // id -> snapshot slot
-  int32_t* winner = nullptr; int64_t cap_winner = 0;
+  unsigned long long* winner = nullptr; int64_t cap_winner = 0;
+  unsigned long long upd_seq = 0;  // update batches (the winner claims' high word)
   // incremental store (delta ticks): slots moved since the store was built
   int32_t* mark = nullptr;     // per slot: epoch of its last recorded move
   int32_t* moved = nullptr;    // moved slots
@@ -1179,7 +1178,7 @@ int snap_reserve(mknn_engine* h, int64_t want) {
   cudaFree(h->ht);
   cudaFree(h->winner);
   MKNN_CUDA_OK(cudaMalloc(&h->ht, sizeof(HashSlot) * hc));
-  MKNN_CUDA_OK(cudaMalloc(&h->winner, sizeof(int32_t) * nc));
+  MKNN_CUDA_OK(cudaMalloc(&h->winner, sizeof(unsigned long long) * nc));
   cudaFree(h->mark);
   cudaFree(h->moved);
   MKNN_CUDA_OK(cudaMalloc(&h->mark, sizeof(int32_t) * nc));
@@ -1196,10 +1195,11 @@ int snap_reserve(mknn_engine* h, int64_t want) {
     MKNN_CUDA_OK(cudaMemsetAsync(h->d_nsnap, 0, 2 * sizeof(int32_t), s));
   }
   MKNN_LAUNCH k_fill_slots<<<gs_blocks(hc), 256, 0, s>>>(h->ht, hc);
-  MKNN_LAUNCH k_fill_i32<<<gs_blocks(nc), 256, 0, s>>>(h->winner, nc, -1);
+  MKNN_CUDA_OK(cudaMemsetAsync(h->winner, 0, sizeof(unsigned long long) * nc, s));
+  h->upd_seq = 0;
   if (h->n_snap)
     MKNN_LAUNCH k_hash_load<<<gs_blocks(h->n_snap), 256, 0, s>>>(h->snap_ids, h->n_snap, h->ht,
-                                                                 (uint64_t)(hc - 1), h->winner);
+                                                                 (uint64_t)(hc - 1));
   MKNN_CUDA_OK(cudaGetLastError());
   return 0;
 }
@@ -1219,7 +1219,7 @@ int snap_load_dev(mknn_engine* h, int64_t n, const long long* ids, const double*
   MKNN_LAUNCH k_fill_slots<<<gs_blocks(h->hcap), 256, 0, s>>>(h->ht, h->hcap);
   if (n)
     MKNN_LAUNCH k_hash_load<<<gs_blocks(n), 256, 0, s>>>(h->snap_ids, n, h->ht,
-                                                         (uint64_t)(h->hcap - 1), h->winner);
+                                                         (uint64_t)(h->hcap - 1));
   MKNN_CUDA_OK(cudaGetLastError());
   h->n_snap = h->n_snap_hi = n;
   h->nmoved_hi = 0;
@@ -1263,18 +1263,23 @@ int snap_update_dev(mknn_engine* h, int64_t nu, const long long* ids, const doub
   if ((rc = grow(h->slot_of, h->cap_slot_of, nu))) return rc;
   cudaStream_t s = h->stream;
   MKNN_CUDA_OK(cudaMemcpyAsync(h->d_nsnap + 1, h->d_nsnap, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  if (++h->upd_seq >= (1ull << 32)) {  // the high word would wrap: start over
+    MKNN_CUDA_OK(cudaMemsetAsync(h->winner, 0, sizeof(unsigned long long) * h->cap_winner, s));
+    h->upd_seq = 1;
+  }
+  const unsigned long long seq = h->upd_seq;
   MKNN_LAUNCH k_update_claim<<<gs_blocks(nu), 256, 0, s>>>(ids, nu, h->ht, (uint64_t)(h->hcap - 1),
-                                               h->d_nsnap, h->winner, h->slot_of);
+                                               h->d_nsnap, h->winner, h->slot_of, seq);
   // a batch above the incremental threshold on its own (engine: > 5 % of
   // the snapshot) sends the next tick to the full re-index anyway: skip the
   // moved-slot bookkeeping (a random read-modify-write per update) and mark
   // the store stale so the incremental path cannot be chosen on a partial list
   const bool track = nu * 20 <= h->n_snap;
   if (!track) h->st.valid = false;
-  MKNN_LAUNCH k_update_apply<<<gs_blocks(nu), 256, 0, s>>>(ids, x, y, nu, h->slot_of, h->winner, h->snap_ids,
+  MKNN_LAUNCH k_update_apply<<<gs_blocks(nu), 256, 0, s>>>(ids, x, y, nu, h->slot_of, h->winner, seq,
+                                               h->snap_ids,
                                                h->snap_x, h->snap_y, h->mark, h->epoch, h->moved,
                                                h->d_nmoved, track, h->d_nsnap + 1);
-  MKNN_LAUNCH k_update_reset<<<gs_blocks(nu), 256, 0, s>>>(nu, h->slot_of, h->winner);
   MKNN_CUDA_OK(cudaGetLastError());
   h->upd_pending = true;
   h->n_snap_hi += nu;
