@@ -2540,7 +2540,12 @@ int search_launch(const SearchArgs& a, cudaStream_t s) {
   // 16 < k <= 32: k_search1 (lists as positions in shared memory, rows
   // written once); k <= 16: the row-resident kernel, measured 3-11 % faster
   // there (the per-visit position gather weighs more on short lists)
-  if (a.k > 16 && a.k <= 32 && !v0) {
+  // MKNN_S1_MIN=k0: k_search1 from k > k0 (A/B; default 16)
+  static const int s1_min = [] {
+    const char* e = getenv("MKNN_S1_MIN");
+    return e ? atoi(e) : 16;
+  }();
+  if (a.k > s1_min && a.k <= 32 && !v0) {
     const double qd = (double)a.nq / (double)(a.n_objects > 0 ? a.n_objects : 1);
     // MKNN_OWN_STAGED=1: the own-leaf pass as k_own1's staged leaf tasks
     // (bulk copies into shared memory) instead of inline in k_search1
