@@ -2496,7 +2496,10 @@ int launch_batched(const SearchArgs& a, cudaStream_t s) {
 }
 
 // resident CTAs of k_search1 per SM (1-warp CTAs; registers bound it)
-constexpr int SEARCH1_CTAS_PER_SM = 32;
+#ifndef MKNN_S1_CTAS
+#define MKNN_S1_CTAS 32
+#endif
+constexpr int SEARCH1_CTAS_PER_SM = MKNN_S1_CTAS;
 
 template <int B, bool FUSED>
 int launch_search1(const SearchArgs& a, cudaStream_t s) {
