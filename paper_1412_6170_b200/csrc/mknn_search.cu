@@ -834,6 +834,20 @@ constexpr bool KCAP = MKNN_KCAP;
 #endif
 constexpr bool EMPTY_SHORTCUT = MKNN_EMPTY_SHORTCUT;
 
+// k > 32: when the buffer is merged.  k <= 128 (KPL <= 4): once it holds
+// more than N - 32 candidates (one network merge per N - 32); k > 128: after
+// every admitting step (always <= 32 candidates, so always the rank merge:
+// the 8- and 16-slot 64-bit networks cost more than the extra merges, k =
+// 256: 49.3 -> 31.8 ms; at k = 128 the same measured 11.2 -> 16.4 ms).
+// -DMKNN_FLUSH_AT=t: merge at more than t candidates for every k (A/B)
+#ifndef MKNN_FLUSH_AT
+#define MKNN_FLUSH_AT -1
+#endif
+template <int KPL>
+__host__ __device__ constexpr int flush_at() {
+  return MKNN_FLUSH_AT >= 0 ? MKNN_FLUSH_AT : (KPL >= 8 ? 0 : 32 * KPL - 32);
+}
+
 #ifndef MKNN_RANK_MERGE
 #define MKNN_RANK_MERGE 32
 #endif
@@ -1012,7 +1026,7 @@ __device__ __forceinline__ void visit_leaf_sm(int k, int leaf, double qx, double
         nbuf += __popc(m);
         prof_add(a.prof, PROF_ADMITTED, __popc(m), lane);
         __syncwarp();
-        if (nbuf > N - 32) {
+        if (nbuf > flush_at<KPL>()) {
           prof_add(a.prof, PROF_SORT_MERGES, 1, lane);
           merge_sm<KPL>(ld, li, bufd, bufi, nbuf, lane);
           nbuf = 0;
